@@ -1,0 +1,381 @@
+#!/usr/bin/env python3
+"""Headline benchmark: bi-level l_{1,inf} projection of the 10000 x 10000 fp32
+matrix (BASELINE.json config 2, U[-1,1], seed 2) over the radius sweep
+eta in {0.001, 0.01, 0.1, 0.5} * ||Y||_{1,inf}, on N GPUs (one process each).
+
+A STEP is one radius sweep: four projections of the resident matrix through
+the C-ABI device entry point (mp_bilevel_project), captured once in a CUDA
+graph.  L2 is flushed (256 MiB memset) before every projection; CUDA events
+around each projection exclude the flush from the timing.  Metric: algorithmic
+GB/s = sum over projections of 4 B * n * m * (2 + f_surv) / device time (one
+full read, a read of the surviving columns, one full write).
+
+`--impl reference` times the reference's own CPU path (oracle/_ref, the
+unmodified reference library compiled from /root/reference, with all host
+threads) on the same metric: each step is one projection, cycling through the
+radii (a bounded sample).  Under torchrun only rank 0 runs it.
+
+Multi-GPU: the path has no data-path exchange for independent matrices, so
+each rank projects its own matrix (weak scaling); the only collective is the
+max-over-ranks reduction of the measured times.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_ROWS, N_COLS = 10000, 10000
+RADII = (0.001, 0.01, 0.1, 0.5)
+SEED = 2
+METRIC = "bi-level ℓ1,∞ projection GB/s and % HBM roofline, 10000×10000 fp32, 1 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def make_input(rank: int):
+    from paper_2405_02086_b200 import datagen
+    # rank 0 uses the BASELINE seed; other ranks project their own matrices
+    return datagen.uniform(SEED + 1000 * rank, (N_ROWS, N_COLS), -1.0, 1.0)
+
+
+def etas_for(y: np.ndarray):
+    colmax = np.abs(y).max(axis=0).astype(np.float64)
+    norm = float(colmax.sum())  # ||Y||_{1,inf} (exact: max is exact, sum in f64)
+    return [r * norm for r in RADII], colmax
+
+
+def algo_bytes(n, m, f_surv, s=4):
+    return s * n * m * (2.0 + f_surv)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        loaded = [v for v in sm if smax and v > 0.5 * max(smax)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_reference_times(y, etas, reps_per_eta=1, workers=None):
+    """Reference CPU path (oracle/_ref when built, else the C restatement)."""
+    from oracle import oracle as O
+    workers = workers or os.cpu_count() or 1
+    if O.ref_available():
+        t = O.ref_time_bilevel(y, etas, "1", "inf", reps=reps_per_eta, workers=workers)
+        return list(t), "reference", workers
+    times = []
+    y64 = y.astype(np.float64)
+    for e in etas:
+        for _ in range(reps_per_eta):
+            t0 = time.perf_counter()
+            O.bilevel(y64, e)
+            times.append(time.perf_counter() - t0)
+    return times, "port", 1
+
+
+def run_reference(args, rank):
+    """--impl reference: the reference's CPU path, rank 0 only."""
+    if rank != 0:
+        return
+    y = make_input(0)
+    etas, colmax = etas_for(y)
+    f_surv = []
+    for e in etas:  # survivors per radius (from the exact outer projection)
+        from oracle import oracle as O
+        u = O.project_ball(colmax, "1", e)
+        f_surv.append(float(np.mean(u > 0)))
+    # warmup + K steps, each one projection cycling through the radii
+    from oracle import oracle as O
+    workers = os.cpu_count() or 1
+    kind = "reference" if O.ref_available() else "port"
+    total_bytes, total_t, per = 0.0, 0.0, []
+    for i in range(args.warmup + args.steps):
+        k = i % len(etas)
+        t, kind, used = cpu_reference_times(y, [etas[k]], 1, workers)
+        if i >= args.warmup:
+            b = algo_bytes(N_ROWS, N_COLS, f_surv[k])
+            total_bytes += b
+            total_t += t[0]
+            per.append(t[0])
+    gbs = total_bytes / total_t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded xoshiro256++ U[-1,1], fp32 values upcast to f64)",
+        "config": {"workload": "config2: bilevel l1,inf 10000x10000, radius sweep",
+                   "radii": list(RADII), "step": "one projection per step, cycling radii"},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": used, "kind": kind,
+                         "sample": f"{args.steps} reference bilevel_project calls (ThreadPool workers={used}), "
+                                   "1 per step cycling the 4 radii; time includes the API's own output copy"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_2405_02086_b200 as mp
+    from paper_2405_02086_b200 import _capi
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = world > 1
+    if dist:
+        import torch.distributed as td
+
+    y_host = make_input(rank)
+    etas, colmax = etas_for(y_host)
+    n, m = y_host.shape
+    y = torch.from_numpy(y_host).to(dev)
+    x = torch.empty_like(y)
+    proj = mp.BilevelProjector(n, m, "float32", "1", "inf", dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream(dev)
+    nproj = len(etas)
+    # events: per projection [start, after K1, after K2, after K3]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nproj)]
+    lib = _capi.lib()
+
+    def one_step():
+        for k, e in enumerate(etas):
+            flush.zero_()
+            handles = (C.c_void_p * 4)(*[C.c_void_p(v.cuda_event) for v in ev[k]])
+            lib.mp_profile_events(handles, 4)
+            proj(y, x, e, stream=stream)
+        lib.mp_profile_events(None, 0)
+
+    with torch.cuda.stream(stream):
+        for v in [ev_ for row in ev for ev_ in row]:
+            v.record(stream)  # materialise the events before capture
+        one_step()  # eager warm call (also loads modules)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            one_step()
+    torch.cuda.synchronize()
+    # survivors per radius (device info after a plain run)
+    f_surv = []
+    for e in etas:
+        proj(y, x, e)
+        torch.cuda.synchronize()
+        inf = proj.info()
+        f_surv.append(inf.survivors / m)
+    bytes_step = sum(algo_bytes(n, m, f) for f in f_surv)
+    apply_bytes = [4.0 * n * m * (1.0 + f) for f in f_surv]  # K3: surviving reads + full write
+
+    for _ in range(max(3, args.warmup)):
+        g.replay()
+    torch.cuda.synchronize()
+    if dist:
+        td.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.15)
+    torch.cuda.synchronize()
+    t_proj = 0.0
+    t_k = [0.0, 0.0, 0.0]
+    t_apply_per = [0.0] * nproj
+    wall0 = torch.cuda.Event(enable_timing=True)
+    wall1 = torch.cuda.Event(enable_timing=True)
+    wall0.record(stream)
+    for _ in range(args.steps):
+        g.replay()
+        stream.synchronize()  # events are re-recorded every replay: read them per step
+        for k in range(nproj):
+            a, b, c, d = ev[k]
+            t_proj += a.elapsed_time(d)
+            t_k[0] += a.elapsed_time(b)
+            t_k[1] += b.elapsed_time(c)
+            t_k[2] += c.elapsed_time(d)
+            t_apply_per[k] += c.elapsed_time(d)
+    wall1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        td.barrier()
+    clock_info = clocks.stop()
+    wall_ms = wall0.elapsed_time(wall1)
+    ms_per_step = t_proj / args.steps
+    if dist:
+        tt = torch.tensor([ms_per_step], dtype=torch.float64, device=dev)
+        td.all_reduce(tt, op=td.ReduceOp.MAX)
+        ms_per_step = float(tt.item())
+    value = world * bytes_step / (ms_per_step * 1e-3) / 1e9
+
+    # ---- dominant kernel roofline: K3 (apply) per launch
+    peak, peak_src = peaks()
+    k3_ms = t_k[2] / (args.steps * nproj)
+    k3_bytes = sum(apply_bytes) / nproj
+    k3_gbs = k3_bytes / (k3_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": k3_gbs, "peak": peak, "unit": "GB/s", "frac": k3_gbs / peak,
+                "traffic": None, "kernel": "k_apply (K3, l_inf clamp)", "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": k3_bytes, "avg_launch_ms": k3_ms}
+    call_gbs = bytes_step / (ms_per_step * 1e-3) / 1e9
+    phase_ms = {"norm_K1": t_k[0] / (args.steps * nproj), "outer_K2": t_k[1] / (args.steps * nproj),
+                "apply_K3": k3_ms}
+    traffic_path = os.path.join(ROOT, "profiles", "k3_traffic.json")
+    if os.path.exists(traffic_path):
+        try:
+            roofline["traffic"] = json.load(open(traffic_path)).get("bytes_per_launch")
+        except Exception:
+            pass
+
+    # ---- e2e through the host-buffer C-ABI entry (pinned host buffers)
+    e2e = None
+    if not args.no_e2e:
+        yh = torch.from_numpy(y_host).pin_memory()
+        xh = torch.empty_like(yh).pin_memory()
+        budgets = np.empty(m, np.float64)
+        z, tau = C.c_int64(), C.c_double()
+        ctx = lib.mp_context_create(local_rank)
+
+        def e2e_step():
+            for e in etas:
+                _capi.check(lib.mp_bilevel_project_host(ctx, yh.data_ptr(), xh.data_ptr(), _capi.MP_F32, n, m, 0, 2,
+                                                        e, budgets.ctypes.data, C.addressof(z), C.addressof(tau), 0))
+        for _ in range(2):
+            e2e_step()
+        e2e_steps = max(3, min(args.steps, 10))
+        if dist:
+            td.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        dt = (time.perf_counter() - t0) / e2e_steps
+        if dist:
+            tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+            td.all_reduce(tt, op=td.ReduceOp.MAX)
+            dt = float(tt.item())
+        lib.mp_context_destroy(ctx)
+        e2e = {"value": world * bytes_step / dt / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": nproj * n * m * 4,
+               "d2h_bytes_per_step": nproj * (n * m * 4 + m * 8 + 48),
+               "ms_per_step": dt * 1e3, "steps": e2e_steps,
+               "path": "mp_bilevel_project_host (pinned host buffers; H2D + kernels + D2H per projection)"}
+
+    # ---- CPU baseline (rank 0, N = 1 only): bounded sample of the workload
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            times, kind, cores = cpu_reference_times(y_host, etas, 1)
+            cb = sum(algo_bytes(n, m, f) for f in f_surv) / sum(times) / 1e9
+            cpu = {"value": cb, "unit": "GB/s", "cores": cores, "kind": kind,
+                   "sample": f"one full radius sweep (4 bilevel_project calls on the 10000x10000 matrix, "
+                             f"f64, workers={cores}); {sum(times):.2f} s total"}
+        except Exception as exc:  # reported, never fatal
+            cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "unavailable", "sample": str(exc)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded xoshiro256++ U[-1,1], BASELINE config 2)",
+            "config": {"workload": "config2: bilevel l1,inf 10000x10000 fp32, radius sweep {0.001,0.01,0.1,0.5}*||Y||",
+                       "step": "4 projections (one per radius), CUDA graph",
+                       "l2": "flushed (256 MiB memset) before every projection; flush excluded by CUDA events",
+                       "f_surv": f_surv, "bytes_per_step": bytes_step,
+                       "pct_hbm_roofline_call": call_gbs / peak, "phase_ms": phase_ms,
+                       "wall_ms_incl_flush": wall_ms, "parallelism": f"replicas x{world}"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clock_info,
+            "gpu_launches": 3 * nproj * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as td
+        torch.cuda.set_device(local_rank)
+        td.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as td
+            td.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,298 @@
+"""B200-native bi-level / multi-level norm-ball projections (arXiv 2405.02086).
+
+Python host mirror of the reference module ``multiproj``
+(proj/python/bindings.cpp:51-137, proj/python/multiproj/__init__.py): same
+function names, argument meaning and error behaviour, computed by the sm_100a
+kernels of ``libmp_b200.so`` through the C-ABI (include/mp_cuda.h).
+
+* numpy inputs take the host path (``mp_*_host``: host->device copy, kernels,
+  device->host copy).  float32 arrays stay float32 (the fp32 device path);
+  anything else is force-cast to float64 like the reference binding
+  (proj/python/bindings.cpp:17-25).
+* torch CUDA tensors take the device path (no copies, current torch stream).
+
+There is no CPU fallback: without the CUDA library every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _capi
+from ._capi import (MP_F32, MP_F64, MP_FLAG_EXACT_ZERO_SIGN, MpInfo, MpConfigError, MpShapeError, MpValueError,
+                    ProjectionError, check, lib, norm_code, parse_norm_spec)
+
+__all__ = [
+    "bilevel_project", "multilevel_project", "trilevel_project_l1infinf", "project_l1", "project_l2",
+    "project_linf", "project_ball", "matrix_pq_norm", "multilevel_norm", "aggregate_leading_axis",
+    "structured_sparsity", "gen_uniform_matrix", "BilevelProjector", "MultilevelProjector",
+    "ProjectionError", "MpValueError", "MpShapeError", "MpConfigError", "MP_FLAG_EXACT_ZERO_SIGN",
+]
+
+
+def _is_torch(a) -> bool:
+    return type(a).__module__.startswith("torch")
+
+
+def _host_array(a) -> np.ndarray:
+    arr = np.asarray(a)
+    if arr.dtype != np.float32:
+        arr = arr.astype(np.float64)
+    return np.ascontiguousarray(arr)
+
+
+def _dt(arr) -> int:
+    if _is_torch(arr):
+        import torch
+        if arr.dtype == torch.float32:
+            return MP_F32
+        if arr.dtype == torch.float64:
+            return MP_F64
+        raise MpConfigError(f"unsupported dtype {arr.dtype}")
+    return MP_F32 if arr.dtype == np.float32 else MP_F64
+
+
+def _ptr(a) -> int:
+    return a.data_ptr() if _is_torch(a) else a.ctypes.data
+
+
+# -------------------------------------------------------------- device path
+class BilevelProjector:
+    """Pre-planned bi-level projection on device tensors.
+
+    Owns its workspace so a call allocates nothing and never syncs: it can be
+    captured in a CUDA graph.  ``__call__(y, x, eta)`` writes x (may be y)."""
+
+    def __init__(self, n: int, m: int, dtype="float32", p="1", q="inf", device=None, flags: int = 0):
+        import torch
+        self.n, self.m = int(n), int(m)
+        self.tdtype = torch.float32 if str(dtype) in ("float32", "torch.float32") else torch.float64
+        self.dt = MP_F32 if self.tdtype == torch.float32 else MP_F64
+        self.p, self.q = norm_code(p), norm_code(q)
+        self.flags = flags
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        wsb = lib().mp_bilevel_workspace_size(self.dt, self.n, self.m, self.p, self.q)
+        if wsb == 0:
+            raise MpShapeError("bilevel_project requires a non-empty order-2 tensor")
+        self.ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
+        self.budgets = torch.empty(self.m, dtype=torch.float64, device=self.device)
+        self.norms = torch.empty(self.m, dtype=torch.float64, device=self.device)
+        self.info_buf = torch.zeros(C.sizeof(MpInfo), dtype=torch.uint8, device=self.device)
+
+    def __call__(self, y, x, eta: float, stream=None):
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(lib().mp_bilevel_project(y.data_ptr(), x.data_ptr(), self.dt, self.n, self.m, self.p, self.q,
+                                       float(eta), self.budgets.data_ptr(), self.norms.data_ptr(),
+                                       self.info_buf.data_ptr(), self.flags, self.ws.data_ptr(), self.ws.numel(),
+                                       s.cuda_stream))
+        return x
+
+    def info(self) -> MpInfo:
+        raw = self.info_buf.cpu().numpy().tobytes()
+        return MpInfo.from_buffer_copy(raw)
+
+
+class MultilevelProjector:
+    """Pre-planned multi-level projection on device tensors (graph capturable)."""
+
+    def __init__(self, shape, levels, dtype="float32", device=None, flags: int = 0):
+        import torch
+        self.shape = [int(s) for s in shape]
+        self.levels = parse_norm_spec(levels)
+        self.tdtype = torch.float32 if str(dtype) in ("float32", "torch.float32") else torch.float64
+        self.dt = MP_F32 if self.tdtype == torch.float32 else MP_F64
+        self.flags = flags
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._shape_c = (C.c_int64 * len(self.shape))(*self.shape)
+        self._lv_c = (C.c_int * max(1, len(self.levels)))(*self.levels)
+        wsb = lib().mp_multilevel_workspace_size(self.dt, self._shape_c, len(self.shape), self._lv_c,
+                                                 len(self.levels))
+        if wsb == 0:
+            # reproduce the reference's error for this spec / shape
+            check(lib().mp_multilevel_project(None, None, self.dt, self._shape_c, len(self.shape), self._lv_c,
+                                              len(self.levels), 0.0, None, None, 0, None, 0, None))
+        self.ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
+        chain = 0
+        for i in range(len(self.shape) - 1, 0, -1):
+            chain += int(np.prod(self.shape[i:]))
+        self.chain = torch.empty(max(1, chain), dtype=torch.float64, device=self.device)
+        self.info_buf = torch.zeros(C.sizeof(MpInfo), dtype=torch.uint8, device=self.device)
+
+    def __call__(self, t, x, eta: float, stream=None):
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(lib().mp_multilevel_project(t.data_ptr(), x.data_ptr(), self.dt, self._shape_c, len(self.shape),
+                                          self._lv_c, len(self.levels), float(eta), self.chain.data_ptr(),
+                                          self.info_buf.data_ptr(), self.flags, self.ws.data_ptr(),
+                                          self.ws.numel(), s.cuda_stream))
+        return x
+
+    def budget_chain(self):
+        out, off = [], 0
+        for i in range(len(self.shape) - 1, 0, -1):
+            size = int(np.prod(self.shape[i:]))
+            out.append(self.chain[off:off + size].reshape(self.shape[i:]))
+            off += size
+        return out
+
+    def info(self) -> MpInfo:
+        return MpInfo.from_buffer_copy(self.info_buf.cpu().numpy().tobytes())
+
+
+# ------------------------------------------------------------ public API
+def bilevel_project(y, eta, p="1", q="inf", workers=1, flags: int = 0):
+    """Bi-level l_{p,q} projection; returns (X, budgets, zero_columns).
+
+    Mirrors ``multiproj.bilevel_project`` (proj/python/bindings.cpp:71-85 ->
+    proj/src/bilevel.cpp:10-32).  ``workers`` is accepted for API
+    compatibility; the CUDA grid replaces the CPU pool."""
+    del workers
+    pc, qc = norm_code(p), norm_code(q)
+    if _is_torch(y):
+        if y.dim() != 2:
+            raise MpShapeError("bilevel_project requires order 2")
+        yc = y.contiguous()
+        proj = BilevelProjector(yc.shape[0], yc.shape[1], yc.dtype, pc, qc, yc.device, flags)
+        x = proj(yc, yc.clone(), eta)
+        info = proj.info()
+        check(info.status)
+        return x, proj.budgets.clone(), int(info.zero_columns)
+    arr = _host_array(y)
+    if arr.ndim != 2:
+        raise MpShapeError("bilevel_project requires order 2")
+    n, m = arr.shape
+    x = np.empty_like(arr)
+    budgets = np.empty(m, np.float64)
+    z, tau = C.c_int64(), C.c_double()
+    check(lib().mp_bilevel_project_host(None, arr.ctypes.data, x.ctypes.data, _dt(arr), n, m, pc, qc, float(eta),
+                                        budgets.ctypes.data, C.addressof(z), C.addressof(tau), flags))
+    return x, budgets.tolist(), int(z.value)
+
+
+def multilevel_project(y, norms, eta, workers=1, flags: int = 0, return_chain: bool = False):
+    """Multi-level projection, norms innermost first (e.g. 'inf,inf,1').
+
+    Mirrors ``multiproj.multilevel_project`` (proj/python/bindings.cpp:87-99
+    -> multilevel_project_iter, proj/src/multilevel.cpp:93-124)."""
+    del workers
+    levels = parse_norm_spec(norms)
+    if _is_torch(y):
+        t = y.contiguous()
+        proj = MultilevelProjector(t.shape, levels, t.dtype, t.device, flags)
+        x = proj(t, t.clone(), eta)
+        check(proj.info().status)
+        return (x, proj.budget_chain()) if return_chain else x
+    arr = _host_array(y)
+    if arr.ndim == 0:
+        raise MpShapeError("tensor order must be >= 1")
+    shape = (C.c_int64 * arr.ndim)(*arr.shape)
+    lv = (C.c_int * max(1, len(levels)))(*levels)
+    x = np.empty_like(arr)
+    sizes = [int(np.prod(arr.shape[i:])) for i in range(arr.ndim - 1, 0, -1)]
+    chain = np.empty(max(1, sum(sizes)), np.float64)
+    check(lib().mp_multilevel_project_host(None, arr.ctypes.data, x.ctypes.data, _dt(arr), shape, arr.ndim, lv,
+                                           len(levels), float(eta), chain.ctypes.data, flags))
+    if not return_chain:
+        return x
+    out, off = [], 0
+    for i, s in zip(range(arr.ndim - 1, 0, -1), sizes):
+        out.append(chain[off:off + s].reshape(arr.shape[i:]))
+        off += s
+    return x, out
+
+
+def trilevel_project_l1infinf(t, eta, workers=1, flags: int = 0):
+    """Named l_{1,inf,inf} path for order-3 tensors (proj/src/multilevel.cpp:126-132)."""
+    nd = t.dim() if _is_torch(t) else np.asarray(t).ndim
+    if nd != 3:
+        raise MpShapeError("trilevel_project_l1infinf requires order 3")
+    return multilevel_project(t, "inf,inf,1", eta, workers, flags)
+
+
+def project_ball(y, q, radius):
+    """Vector-ball projection (proj/src/vector_balls.cpp:207-214)."""
+    qc = norm_code(q)
+    arr = _host_array(y).reshape(-1)
+    x = np.empty_like(arr)
+    check(lib().mp_project_ball_host(None, arr.ctypes.data, x.ctypes.data, _dt(arr), arr.size, qc, float(radius)))
+    return x
+
+
+def project_l1(y, radius):
+    return project_ball(y, "1", radius)
+
+
+def project_l2(y, radius):
+    return project_ball(y, "2", radius)
+
+
+def project_linf(y, radius):
+    return project_ball(y, "inf", radius)
+
+
+def aggregate_leading_axis(t, q):
+    """out[f] = ||fiber f||_q over the leading axis (proj/src/tensor.cpp:107-138)."""
+    arr = _host_array(t)
+    if arr.ndim < 2:
+        raise MpShapeError("aggregate_leading_axis requires order >= 2")
+    n = arr.shape[0]
+    m = arr.size // n
+    out = np.empty(m, np.float64)
+    check(lib().mp_aggregate_host(None, arr.ctypes.data, out.ctypes.data, _dt(arr), n, m, norm_code(q)))
+    return out.reshape(arr.shape[1:])
+
+
+def _vector_norm(v: np.ndarray, q: int) -> float:
+    # proj/src/tensor.cpp:78-99 on the (small) final aggregate
+    if not np.all(np.isfinite(v)):
+        raise MpValueError("non-finite vector entry")
+    a = np.abs(v.astype(np.float64).reshape(-1))
+    if q == 0:
+        return float(np.sum(a))
+    if q == 1:
+        return float(np.sqrt(np.sum(a * a)))
+    return float(np.max(a)) if a.size else 0.0
+
+
+def multilevel_norm(y, norms) -> float:
+    """Nested-norm value (proj/src/multilevel.cpp:134-141)."""
+    levels = parse_norm_spec(norms)
+    arr = _host_array(y)
+    if len(levels) != arr.ndim:
+        raise MpShapeError("norm spec depth does not match tensor order")
+    if not np.all(np.isfinite(arr)):
+        raise MpValueError("non-finite tensor entry")
+    cur = arr
+    for q in levels[:-1]:
+        cur = aggregate_leading_axis(cur, q)
+    return _vector_norm(cur, levels[-1])
+
+
+def matrix_pq_norm(y, p, q) -> float:
+    """||Y||_{p,q} (proj/src/tensor.cpp:101-105)."""
+    arr = _host_array(y)
+    if arr.ndim != 2:
+        raise MpShapeError("matrix_pq_norm requires order 2")
+    return multilevel_norm(arr, [norm_code(q), norm_code(p)])
+
+
+def structured_sparsity(y, tol=0.0):
+    """(zero_columns, fraction) of columns with max |x| <= tol (proj/src/tensor.cpp:152-164)."""
+    arr = _host_array(y)
+    if arr.ndim != 2:
+        raise MpShapeError("structured_sparsity requires order 2")
+    mx = aggregate_leading_axis(arr, "inf")
+    count = int(np.sum(mx <= tol))
+    return count, count / arr.shape[1]
+
+
+def gen_uniform_matrix(n, m, seed, lo=0.0, hi=1.0):
+    """Deterministic uniform matrix (proj/src/rng.cpp:64-79), via datagen."""
+    from . import datagen
+    if n < 1 or m < 1:
+        raise MpConfigError("matrix dims must be >= 1")
+    if not lo < hi:
+        raise MpConfigError("uniform bounds require lo < hi")
+    return datagen.uniform(seed, (n, m), lo, hi, dtype=np.float64)

@@ -1,0 +1,55 @@
+"""In-tree build of the native libraries (sm_100a only).
+
+* ``libmp_b200.so``   -- the CUDA kernels + C-ABI (include/mp_cuda.h).
+* ``libmp_datagen.so`` -- seeded synthetic-input generator (harness).
+
+Both are built IN-TREE next to this file so they travel with the repo
+snapshot to the GPU box (``*.so`` is git-ignored, not gpurun-ignored).
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+LIB = os.path.join(PKG, "libmp_b200.so")
+DATAGEN = os.path.join(PKG, "libmp_datagen.so")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+    "-shared",
+]
+CU_SOURCES = ["mp_device.cu", "mp_host.cu"]
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> None:
+    deps = glob.glob(os.path.join(CSRC, "*")) + [os.path.join(INCLUDE, "mp_cuda.h")]
+    if force or _stale(LIB, deps):
+        cmd = [NVCC, *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}",
+               *[os.path.join(CSRC, s) for s in CU_SOURCES], "-o", LIB + ".tmp"]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+        os.replace(LIB + ".tmp", LIB)
+    dg = os.path.join(CSRC, "datagen.c")
+    if force or _stale(DATAGEN, [dg]):
+        subprocess.run(["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fPIC", "-shared", dg,
+                        "-o", DATAGEN, "-lm"], check=True)
+
+
+if __name__ == "__main__":
+    build(force=True, verbose=True)

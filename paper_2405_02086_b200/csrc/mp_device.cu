@@ -1,0 +1,576 @@
+// mp_device.cu -- device entry points of the C-ABI (include/mp_cuda.h):
+// argument validation (reference exception taxonomy), workspace carving,
+// grid planning and kernel dispatch.  No allocation, no host sync: every
+// entry point is stream-ordered and CUDA-graph capturable.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <mutex>
+#include <vector>
+
+#include "mp_internal.h"
+#include "mp_kernels.cuh"
+#include "mp_l1strip.cuh"
+#include "mp_outer_large.cuh"
+
+namespace mpi {
+
+static thread_local std::string g_err;
+static thread_local cudaEvent_t g_prof[4] = {nullptr, nullptr, nullptr, nullptr};
+
+void prof_mark(int i, cudaStream_t s) {
+  if (g_prof[i]) cudaEventRecord(g_prof[i], s);
+}
+
+void set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+const char* last_error() { return g_err.c_str(); }
+
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (cached[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cached[dev] = v;
+  }
+  return cached[dev];
+}
+
+}  // namespace mpi
+
+using namespace mpi;
+
+namespace {
+
+// ----------------------------------------------------------- grid planning
+struct Grid {
+  int vec = 1;
+  int threads = 32;
+  int64_t ntiles = 1;  // column tiles (grid.x)
+  int64_t nrb = 1;     // row blocks (grid.y)
+  int64_t rpb = 1;     // rows per block
+};
+
+Grid plan_grid(int vec, int64_t n, int64_t m) {
+  Grid g;
+  g.vec = vec;
+  const int64_t slots = (m + vec - 1) / vec;
+  g.threads = static_cast<int>(std::min<int64_t>(mpk::kThreads, ((slots + 31) / 32) * 32));
+  g.ntiles = (slots + g.threads - 1) / g.threads;
+  // ~2048 resident threads per SM: enough 16-byte loads in flight to cover
+  // HBM latency (U loads per thread), grid a whole multiple of the SM count.
+  const int64_t target_ctas = static_cast<int64_t>(sm_count()) * (2048 / g.threads);
+  int64_t nrb = (target_ctas + g.ntiles - 1) / g.ntiles;
+  nrb = std::max<int64_t>(1, std::min<int64_t>(nrb, (n + 3) / 4));
+  nrb = std::min<int64_t>(nrb, 65535);
+  g.rpb = (n + nrb - 1) / nrb;
+  g.nrb = (n + g.rpb - 1) / g.rpb;
+  return g;
+}
+
+int pick_vec(mp_dtype dt, int64_t m, const void* a, const void* b) {
+  const uintptr_t al = reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b);
+  if (dt == MP_F32) {
+    if (m % 4 == 0 && al % 16 == 0) return 4;
+    if (m % 2 == 0 && al % 8 == 0) return 2;
+    return 1;
+  }
+  if (m % 2 == 0 && al % 16 == 0) return 2;
+  return 1;
+}
+
+// Largest row-block count over every vector width the plan may pick.
+int64_t max_nrb(mp_dtype dt, int64_t n, int64_t m) {
+  int64_t r = 1;
+  for (int v : {1, 2, 4}) {
+    if (dt == MP_F64 && v == 4) continue;
+    r = std::max(r, plan_grid(v, n, m).nrb);
+  }
+  return r;
+}
+
+// --------------------------------------------------------------- dispatch
+template <typename T, int VEC>
+cudaError_t launch_colnorm_v(int q, const Grid& g, const T* y, int64_t n, int64_t m, void* out, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(g.ntiles), static_cast<unsigned>(g.nrb));
+  constexpr int U = 8;
+  if (q == mpk::kInf) mpk::k_colnorm<T, VEC, mpk::kInf, U><<<grid, g.threads, 0, s>>>(y, n, m, g.rpb, out);
+  else if (q == mpk::kL1) mpk::k_colnorm<T, VEC, mpk::kL1, U><<<grid, g.threads, 0, s>>>(y, n, m, g.rpb, out);
+  else mpk::k_colnorm<T, VEC, mpk::kL2, U><<<grid, g.threads, 0, s>>>(y, n, m, g.rpb, out);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_colnorm(int q, const Grid& g, const T* y, int64_t n, int64_t m, void* out, cudaStream_t s) {
+  if (g.vec == 4) {
+    if constexpr (sizeof(T) == 4) return launch_colnorm_v<T, 4>(q, g, y, n, m, out, s);
+  }
+  if (g.vec == 2) return launch_colnorm_v<T, 2>(q, g, y, n, m, out, s);
+  return launch_colnorm_v<T, 1>(q, g, y, n, m, out, s);
+}
+
+template <typename T, int VEC>
+cudaError_t launch_apply_v(int q, const Grid& g, const T* y, T* x, int64_t n, int64_t m, const void* colp,
+                           const double* budgets, const mp_info* info, unsigned flags, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(g.ntiles), static_cast<unsigned>(g.nrb));
+  constexpr int U = 4;
+  if (q == mpk::kInf)
+    mpk::k_apply<T, VEC, mpk::kInf, U><<<grid, g.threads, 0, s>>>(y, x, n, m, g.rpb, static_cast<int>(g.nrb), colp,
+                                                                   budgets, info, flags);
+  else
+    mpk::k_apply<T, VEC, mpk::kL2, U><<<grid, g.threads, 0, s>>>(y, x, n, m, g.rpb, static_cast<int>(g.nrb), colp,
+                                                                  budgets, info, flags);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_apply(int q, const Grid& g, const T* y, T* x, int64_t n, int64_t m, const void* colp,
+                         const double* budgets, const mp_info* info, unsigned flags, cudaStream_t s) {
+  if (g.vec == 4) {
+    if constexpr (sizeof(T) == 4) return launch_apply_v<T, 4>(q, g, y, x, n, m, colp, budgets, info, flags, s);
+  }
+  if (g.vec == 2) return launch_apply_v<T, 2>(q, g, y, x, n, m, colp, budgets, info, flags, s);
+  return launch_apply_v<T, 1>(q, g, y, x, n, m, colp, budgets, info, flags, s);
+}
+
+cudaError_t outer_setup() {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(mpk::k_outer, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(mpk::kOuterMaxM * sizeof(double)));
+    if (err == cudaSuccess) err = mpk::l1strip_setup();
+  });
+  return err;
+}
+
+cudaError_t launch_outer(const mpk::OuterArgs& a, cudaStream_t s) {
+  cudaError_t e = outer_setup();
+  if (e != cudaSuccess) return e;
+  const size_t smem = static_cast<size_t>(std::max<int64_t>(a.m, 1)) * sizeof(double);
+  mpk::k_outer<<<1, mpk::kOuterThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+// Column parameters for a fiber projection from (norms v, budgets u).
+template <typename T>
+__global__ void k_colparams(const double* __restrict__ v, const double* __restrict__ u, int64_t m, int q,
+                            void* __restrict__ colp, const mp_info* __restrict__ info) {
+  if (info->status != MP_OK) return;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= m) return;
+  const double uu = u[c];
+  if (q == mpk::kInf) {
+    if constexpr (sizeof(T) == 4)
+      static_cast<float2*>(colp)[c] = make_float2(__double2float_rz(uu), __double2float_rn(uu));
+    else
+      static_cast<double*>(colp)[c] = uu;
+  } else if (q == mpk::kL2) {
+    static_cast<double*>(colp)[c] = (v[c] > uu) ? uu / v[c] : 1.0;
+  }
+}
+
+// ------------------------------------------------------ workspace layouts
+struct BilevelWs {
+  mp_info* info;
+  void* k1out;       // l_inf bits or l1/l2 partials
+  double* v;         // norms (f64)
+  double* budgets;   // outer-projected radii
+  void* colp;        // per-column apply parameters
+  mpk::L1StripWs l1; // l1 inner projection scratch
+  void* large;       // k_outer_large scratch (m > kOuterMaxM)
+};
+
+BilevelWs carve_bilevel(Carve& c, mp_dtype dt, int64_t n, int64_t m, mp_norm q) {
+  BilevelWs w{};
+  w.info = c.take<mp_info>(1);
+  if (q == MP_NORM_INF) w.k1out = c.take<unsigned long long>(m);
+  else w.k1out = c.take<double>(static_cast<size_t>(max_nrb(dt, n, m)) * m);
+  w.v = c.take<double>(m);
+  w.budgets = c.take<double>(m);
+  w.colp = c.take<double>(m);
+  if (q == MP_NORM_L1) w.l1 = mpk::carve_l1strip(c, m);
+  w.large = c.take<char>(mpk::outer_large_ws_bytes(m));
+  return w;
+}
+
+// Core of a fiber-projection level: y (T, (n, m)) -> x given norms v and
+// budgets u; colp must hold the per-column parameters for q.
+template <typename T>
+cudaError_t project_fibers(const T* y, T* x, int64_t n, int64_t m, int q, const double* v, const double* u,
+                           const void* colp, const mpk::L1StripWs& l1, const mp_info* info, unsigned flags,
+                           mp_dtype dt, cudaStream_t s) {
+  if (q == mpk::kL1) return mpk::launch_l1strip<T>(y, x, n, m, v, u, l1, info, flags, s);
+  Grid g = plan_grid(pick_vec(dt, m, y, x), n, m);
+  return launch_apply<T>(q, g, y, x, n, m, colp, u, info, flags, s);
+}
+
+template <typename T>
+mp_status bilevel_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, mp_norm p, mp_norm q, double eta,
+                       double* budgets, double* norms, mp_info* info, unsigned flags, void* ws, size_t wsb,
+                       cudaStream_t s) {
+  Carve c(ws, wsb);
+  BilevelWs w = carve_bilevel(c, dt, n, m, q);
+  if (!c.fits()) return fail(MP_ERR_WORKSPACE, "mp_bilevel_project: workspace too small");
+  mp_info* inf = info ? info : w.info;
+  double* u = budgets ? budgets : w.budgets;
+  double* v = norms ? norms : w.v;
+
+  const Grid g = plan_grid(pick_vec(dt, m, y, x), n, m);
+  prof_mark(0, s);
+  mpk::OuterArgs oa{};
+  oa.m = m;
+  oa.p = p;
+  oa.eta = eta;
+  oa.u_out = u;
+  oa.info = inf;
+  oa.scratch = w.large;
+  if (q == MP_NORM_INF) {
+    MP_CUDA_TRY(cudaMemsetAsync(w.k1out, 0, static_cast<size_t>(m) * sizeof(unsigned long long), s));
+    MP_CUDA_TRY(launch_colnorm<T>(q, g, y, n, m, w.k1out, s));
+    oa.vin = w.k1out;
+    oa.vkind = sizeof(T) == 4 ? 0 : 1;  // f64 |y| bits are the f64 values
+    oa.v_out = (norms || sizeof(T) == 8) ? v : nullptr;
+    if constexpr (sizeof(T) == 4) oa.rdrn = static_cast<float2*>(w.colp);
+    else oa.v_out = v;  // the apply reads budgets directly; keep v for symmetry
+  } else {
+    MP_CUDA_TRY(launch_colnorm<T>(q, g, y, n, m, w.k1out, s));
+    const int fin_threads = 256;
+    const unsigned fin_blocks = static_cast<unsigned>((m + fin_threads - 1) / fin_threads);
+    if (q == MP_NORM_L1)
+      mpk::k_colnorm_finalize<mpk::kL1><<<fin_blocks, fin_threads, 0, s>>>(w.k1out, g.nrb, m, 0, v);
+    else
+      mpk::k_colnorm_finalize<mpk::kL2><<<fin_blocks, fin_threads, 0, s>>>(w.k1out, g.nrb, m, 0, v);
+    MP_CUDA_TRY(cudaGetLastError());
+    oa.vin = v;
+    oa.vkind = 1;
+    if (q == MP_NORM_L2) oa.factor = static_cast<double*>(w.colp);
+  }
+  prof_mark(1, s);
+  if (m > mpk::kOuterMaxM) {
+    MP_CUDA_TRY(mpk::launch_outer_large(oa, s));
+  } else {
+    MP_CUDA_TRY(launch_outer(oa, s));
+  }
+  prof_mark(2, s);
+  const void* colp = (q == MP_NORM_INF && sizeof(T) == 8) ? static_cast<const void*>(u) : w.colp;
+  MP_CUDA_TRY(project_fibers<T>(y, x, n, m, q, v, u, colp, w.l1, inf, flags, dt, s));
+  prof_mark(3, s);
+  return MP_OK;
+}
+
+mp_status check_bilevel_args(const void* y, const void* x, mp_dtype dt, int64_t n, int64_t m, mp_norm p, mp_norm q,
+                             double eta) {
+  if (!dtype_ok(dt)) return fail(MP_ERR_CONFIG, "unknown dtype code");
+  if (!norm_ok(p) || !norm_ok(q)) return fail(MP_ERR_CONFIG, "unknown norm code");
+  if (n < 1 || m < 1) return fail(MP_ERR_SHAPE, "bilevel_project requires a non-empty order-2 tensor");
+  if (!(eta >= 0.0) || !std::isfinite(eta)) return fail(MP_ERR_VALUE, "radius must be a finite nonnegative real");
+  if (!y || !x) return fail(MP_ERR_WORKSPACE, "null tensor pointer");
+  return MP_OK;
+}
+
+
+// --------------------------------------------------------- vector / aggregate
+template <typename T>
+__global__ void k_cast_from_f64(const double* __restrict__ in, T* __restrict__ out, int64_t len,
+                                const mp_info* __restrict__ info) {
+  if (info->status != MP_OK) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < len) out[i] = static_cast<T>(in[i]);
+}
+
+struct VectorWs {
+  mp_info* info;
+  double* u;     // f64 result staging (f32 data)
+  void* large;
+};
+
+VectorWs carve_vector(Carve& c, mp_dtype dt, int64_t len) {
+  VectorWs w{};
+  w.info = c.take<mp_info>(1);
+  w.u = dt == MP_F32 ? c.take<double>(len) : nullptr;
+  w.large = c.take<char>(mpk::outer_large_ws_bytes(len));
+  return w;
+}
+
+// project_ball on a flat vector (proj/src/vector_balls.cpp:207-214).
+mp_status vector_impl(const void* y, void* x, mp_dtype dt, int64_t len, mp_norm q, double radius, mp_info* info,
+                      VectorWs& w, cudaStream_t s) {
+  mp_info* inf = info ? info : w.info;
+  mpk::OuterArgs oa{};
+  oa.vin = y;
+  oa.vkind = dt == MP_F32 ? 2 : 1;
+  oa.m = len;
+  oa.p = q;
+  oa.eta = radius;
+  oa.u_out = dt == MP_F32 ? w.u : static_cast<double*>(x);
+  oa.info = inf;
+  oa.scratch = w.large;
+  if (len > mpk::kOuterMaxM) {
+    MP_CUDA_TRY(mpk::launch_outer_large(oa, s));
+  } else {
+    MP_CUDA_TRY(launch_outer(oa, s));
+  }
+  if (dt == MP_F32) {
+    const unsigned blocks = static_cast<unsigned>((len + 255) / 256);
+    k_cast_from_f64<float><<<blocks, 256, 0, s>>>(w.u, static_cast<float*>(x), len, inf);
+    MP_CUDA_TRY(cudaGetLastError());
+  }
+  return MP_OK;
+}
+
+// Leading-axis aggregate of (n, m) T data into out (f64), via K1 (+ finalize).
+// scratch: l_inf -> m u32/u64 bits (f32 only; f64 bits land in out directly),
+// l1/l2 -> max_nrb * m partials.
+template <typename T>
+mp_status aggregate_impl(const T* t, double* out, mp_dtype dt, int64_t n, int64_t m, int q, void* scratch,
+                         cudaStream_t s) {
+  const Grid g = plan_grid(pick_vec(dt, m, t, t), n, m);
+  const unsigned fin_blocks = static_cast<unsigned>((m + 255) / 256);
+  if (q == mpk::kInf) {
+    void* bits = sizeof(T) == 8 ? static_cast<void*>(out) : scratch;
+    MP_CUDA_TRY(cudaMemsetAsync(bits, 0, static_cast<size_t>(m) * sizeof(T), s));
+    MP_CUDA_TRY(launch_colnorm<T>(q, g, t, n, m, bits, s));
+    if (sizeof(T) == 4) mpk::k_colnorm_finalize<mpk::kInf><<<fin_blocks, 256, 0, s>>>(bits, 1, m, 0, out);
+  } else {
+    MP_CUDA_TRY(launch_colnorm<T>(q, g, t, n, m, scratch, s));
+    if (q == mpk::kL1) mpk::k_colnorm_finalize<mpk::kL1><<<fin_blocks, 256, 0, s>>>(scratch, g.nrb, m, 0, out);
+    else mpk::k_colnorm_finalize<mpk::kL2><<<fin_blocks, 256, 0, s>>>(scratch, g.nrb, m, 0, out);
+  }
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
+size_t aggregate_scratch_bytes(mp_dtype dt, int64_t n, int64_t m, int q) {
+  if (q == mpk::kInf) return static_cast<size_t>(m) * 8;
+  return static_cast<size_t>(max_nrb(dt, n, m)) * static_cast<size_t>(m) * 8;
+}
+
+// ------------------------------------------------------------- multilevel
+struct MultiWs {
+  mp_info* info = nullptr;
+  std::vector<double*> agg;   // agg[i], i = 1..order-1 (agg[0] unused)
+  std::vector<double*> bud;   // budgets B_i (when no user chain), i = 1..order-1
+  void* scratch = nullptr;    // K1 scratch, max over levels
+  void* colp = nullptr;       // per-column params, max M_1..M_{order-1}
+  mpk::L1StripWs l1{};
+  void* large = nullptr;
+  VectorWs vec{};             // depth-1 path
+};
+
+MultiWs carve_multi(Carve& c, mp_dtype dt, const int64_t* shape, int order, const mp_norm* levels) {
+  MultiWs w;
+  std::vector<int64_t> M(order + 1, 1);
+  for (int i = order - 1; i >= 0; --i) M[i] = M[i + 1] * shape[i];
+  if (order == 1) {
+    w.vec = carve_vector(c, dt, M[0]);
+    return w;
+  }
+  w.info = c.take<mp_info>(1);
+  w.agg.assign(order, nullptr);
+  w.bud.assign(order, nullptr);
+  size_t scr = 0;
+  int64_t mmax = 1;
+  for (int i = 1; i < order; ++i) {
+    w.agg[i] = c.take<double>(M[i]);
+    w.bud[i] = c.take<double>(M[i]);
+    mmax = std::max(mmax, M[i]);
+    scr = std::max(scr, aggregate_scratch_bytes(i == 1 ? dt : MP_F64, shape[i - 1], M[i], levels[i - 1]));
+  }
+  w.scratch = c.take<char>(scr);
+  w.colp = c.take<double>(mmax);
+  w.l1 = mpk::carve_l1strip(c, mmax);
+  w.large = c.take<char>(mpk::outer_large_ws_bytes(shape[order - 1]));
+  return w;
+}
+
+template <typename T>
+cudaError_t launch_colparams(const double* v, const double* u, int64_t m, int q, void* colp, const mp_info* info,
+                             cudaStream_t s) {
+  if (q == mpk::kL1) return cudaSuccess;
+  const unsigned blocks = static_cast<unsigned>((m + 255) / 256);
+  k_colparams<T><<<blocks, 256, 0, s>>>(v, u, m, q, colp, info);
+  return cudaGetLastError();
+}
+
+template <typename T>
+mp_status multilevel_impl(const T* t, T* x, mp_dtype dt, const int64_t* shape, int order, const mp_norm* levels,
+                          double eta, double* chain, mp_info* info, unsigned flags, void* ws, size_t wsb,
+                          cudaStream_t s) {
+  Carve c(ws, wsb);
+  MultiWs w = carve_multi(c, dt, shape, order, levels);
+  if (!c.fits()) return fail(MP_ERR_WORKSPACE, "mp_multilevel_project: workspace too small");
+  if (order == 1) return vector_impl(t, x, dt, shape[0], levels[0], eta, info, w.vec, s);
+
+  std::vector<int64_t> M(order + 1, 1);
+  for (int i = order - 1; i >= 0; --i) M[i] = M[i + 1] * shape[i];
+  mp_info* inf = info ? info : w.info;
+  // Budget buffers: inside the user chain when given (deepest first).
+  std::vector<double*> B(order, nullptr);
+  {
+    int64_t off = 0;
+    for (int i = order - 1; i >= 1; --i) {
+      B[i] = chain ? chain + off : w.bud[i];
+      off += M[i];
+    }
+  }
+  // Aggregation chain (proj/src/multilevel.cpp:99-104).
+  mp_status st = aggregate_impl<T>(t, w.agg[1], dt, shape[0], M[1], levels[0], w.scratch, s);
+  if (st != MP_OK) return st;
+  for (int i = 1; i + 1 < order; ++i) {
+    st = aggregate_impl<double>(w.agg[i], w.agg[i + 1], MP_F64, shape[i], M[i + 1], levels[i], w.scratch, s);
+    if (st != MP_OK) return st;
+  }
+  // Deepest aggregate: vector-ball projection at eta (:106-111).
+  mpk::OuterArgs oa{};
+  oa.vin = w.agg[order - 1];
+  oa.vkind = 1;
+  oa.m = M[order - 1];
+  oa.p = levels[order - 1];
+  oa.eta = eta;
+  oa.u_out = B[order - 1];
+  oa.info = inf;
+  oa.scratch = w.large;
+  if (oa.m > mpk::kOuterMaxM) {
+    MP_CUDA_TRY(mpk::launch_outer_large(oa, s));
+  } else {
+    MP_CUDA_TRY(launch_outer(oa, s));
+  }
+  // Unwind (:113-119): level i fibers at the budgets of level i+1.
+  for (int i = order - 2; i >= 1; --i) {
+    MP_CUDA_TRY(launch_colparams<double>(w.agg[i + 1], B[i + 1], M[i + 1], levels[i], w.colp, inf, s));
+    MP_CUDA_TRY(project_fibers<double>(w.agg[i], B[i], shape[i], M[i + 1], levels[i], w.agg[i + 1], B[i + 1],
+                                       w.colp, w.l1, inf, 0u, MP_F64, s));
+  }
+  MP_CUDA_TRY(launch_colparams<T>(w.agg[1], B[1], M[1], levels[0], w.colp, inf, s));
+  MP_CUDA_TRY(project_fibers<T>(t, x, shape[0], M[1], levels[0], w.agg[1], B[1], w.colp, w.l1, inf, flags, dt, s));
+  return MP_OK;
+}
+
+mp_status check_multi_args(const void* t, const void* x, mp_dtype dt, const int64_t* shape, int order,
+                           const mp_norm* levels, int depth, double eta) {
+  if (!dtype_ok(dt)) return fail(MP_ERR_CONFIG, "unknown dtype code");
+  if (!shape || order < 1) return fail(MP_ERR_SHAPE, "tensor order must be >= 1");
+  for (int i = 0; i < order; ++i)
+    if (shape[i] < 1) return fail(MP_ERR_SHAPE, "zero dimension in shape");
+  if (depth < 1 || !levels) return fail(MP_ERR_CONFIG, "empty norm spec");
+  for (int i = 0; i < depth; ++i)
+    if (!norm_ok(levels[i])) return fail(MP_ERR_CONFIG, "unknown norm code");
+  if (depth != order) return fail(MP_ERR_SHAPE, "norm spec depth does not match tensor order");
+  if (!(eta >= 0.0) || !std::isfinite(eta)) return fail(MP_ERR_VALUE, "radius must be a finite nonnegative real");
+  if (!t || !x) return fail(MP_ERR_WORKSPACE, "null tensor pointer");
+  return MP_OK;
+}
+
+}  // namespace
+
+// ================================================================== C-ABI
+extern "C" {
+
+const char* mp_last_error(void) { return last_error(); }
+
+void mp_profile_events(void* const* events, int count) {
+  for (int i = 0; i < 4; ++i)
+    g_prof[i] = (events && i < count) ? static_cast<cudaEvent_t>(events[i]) : nullptr;
+}
+
+int mp_version(void) { return 100; }
+
+size_t mp_bilevel_workspace_size(mp_dtype dtype, int64_t n, int64_t m, mp_norm p, mp_norm q) {
+  (void)p;
+  if (n < 1 || m < 1 || !dtype_ok(dtype) || !norm_ok(q)) return 0;
+  Carve c(nullptr, 0);
+  carve_bilevel(c, dtype, n, m, q);
+  return c.off + 256;
+}
+
+mp_status mp_bilevel_project(const void* y, void* x, mp_dtype dtype, int64_t n, int64_t m, mp_norm p, mp_norm q,
+                             double eta, double* budgets, double* norms, mp_info* info, unsigned flags,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+  mp_status st = check_bilevel_args(y, x, dtype, n, m, p, q, eta);
+  if (st != MP_OK) return st;
+  if (!workspace) return fail(MP_ERR_WORKSPACE, "null workspace");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == MP_F32)
+    return bilevel_impl<float>(static_cast<const float*>(y), static_cast<float*>(x), dtype, n, m, p, q, eta, budgets,
+                               norms, info, flags, workspace, workspace_bytes, s);
+  return bilevel_impl<double>(static_cast<const double*>(y), static_cast<double*>(x), dtype, n, m, p, q, eta, budgets,
+                              norms, info, flags, workspace, workspace_bytes, s);
+}
+
+
+size_t mp_multilevel_workspace_size(mp_dtype dtype, const int64_t* shape, int order, const mp_norm* levels,
+                                    int depth) {
+  if (check_multi_args(reinterpret_cast<void*>(1), reinterpret_cast<void*>(1), dtype, shape, order, levels, depth,
+                       0.0) != MP_OK)
+    return 0;
+  Carve c(nullptr, 0);
+  carve_multi(c, dtype, shape, order, levels);
+  return c.off + 256;
+}
+
+mp_status mp_multilevel_project(const void* t, void* x, mp_dtype dtype, const int64_t* shape, int order,
+                                const mp_norm* levels, int depth, double eta, double* budget_chain, mp_info* info,
+                                unsigned flags, void* workspace, size_t workspace_bytes, void* stream) {
+  mp_status st = check_multi_args(t, x, dtype, shape, order, levels, depth, eta);
+  if (st != MP_OK) return st;
+  if (!workspace) return fail(MP_ERR_WORKSPACE, "null workspace");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == MP_F32)
+    return multilevel_impl<float>(static_cast<const float*>(t), static_cast<float*>(x), dtype, shape, order, levels,
+                                  eta, budget_chain, info, flags, workspace, workspace_bytes, s);
+  return multilevel_impl<double>(static_cast<const double*>(t), static_cast<double*>(x), dtype, shape, order, levels,
+                                 eta, budget_chain, info, flags, workspace, workspace_bytes, s);
+}
+
+size_t mp_project_ball_workspace_size(mp_dtype dtype, int64_t len, mp_norm q) {
+  if (len < 1 || !dtype_ok(dtype) || !norm_ok(q)) return 0;
+  Carve c(nullptr, 0);
+  carve_vector(c, dtype, len);
+  return c.off + 256;
+}
+
+mp_status mp_project_ball(const void* y, void* x, mp_dtype dtype, int64_t len, mp_norm q, double radius,
+                          mp_info* info, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!dtype_ok(dtype)) return fail(MP_ERR_CONFIG, "unknown dtype code");
+  if (!norm_ok(q)) return fail(MP_ERR_CONFIG, "unknown norm code");
+  if (!(radius >= 0.0) || !std::isfinite(radius)) return fail(MP_ERR_VALUE, "radius must be a finite nonnegative real");
+  if (len < 1) return fail(MP_ERR_SHAPE, "empty vector");
+  if (!y || !x || !workspace) return fail(MP_ERR_WORKSPACE, "null pointer");
+  Carve c(workspace, workspace_bytes);
+  VectorWs w = carve_vector(c, dtype, len);
+  if (!c.fits()) return fail(MP_ERR_WORKSPACE, "mp_project_ball: workspace too small");
+  return vector_impl(y, x, dtype, len, q, radius, info, w, static_cast<cudaStream_t>(stream));
+}
+
+size_t mp_aggregate_workspace_size(mp_dtype dtype, int64_t n, int64_t m, mp_norm q) {
+  if (n < 1 || m < 1 || !dtype_ok(dtype) || !norm_ok(q)) return 0;
+  return aggregate_scratch_bytes(dtype, n, m, q) + 256;
+}
+
+mp_status mp_aggregate(const void* t, double* out, mp_dtype dtype, int64_t n, int64_t m, mp_norm q, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+  if (!dtype_ok(dtype)) return fail(MP_ERR_CONFIG, "unknown dtype code");
+  if (!norm_ok(q)) return fail(MP_ERR_CONFIG, "unknown norm code");
+  if (n < 1 || m < 1) return fail(MP_ERR_SHAPE, "aggregate requires a non-empty tensor of order >= 2");
+  if (!t || !out || !workspace) return fail(MP_ERR_WORKSPACE, "null pointer");
+  if (workspace_bytes < aggregate_scratch_bytes(dtype, n, m, q)) return fail(MP_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == MP_F32)
+    return aggregate_impl<float>(static_cast<const float*>(t), out, dtype, n, m, q, workspace, s);
+  return aggregate_impl<double>(static_cast<const double*>(t), out, dtype, n, m, q, workspace, s);
+}
+
+}  // extern "C"

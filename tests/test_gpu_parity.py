@@ -1,0 +1,288 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Small and medium sizes are compared element-wise with the §8(c) rule
+(tests/parity.py); BASELINE.json full sizes are checked element-wise where the
+oracle finishes in seconds and otherwise through size-independent properties
+(feasibility, idempotence, determinism, in-place == out-of-place).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_2405_02086_b200 as mp
+from oracle import oracle as O
+from paper_2405_02086_b200 import datagen
+from tests.parity import check_bilevel
+
+pytestmark = pytest.mark.gpu
+
+bit_equal = lambda a, b: np.array_equal(np.ascontiguousarray(a).view(np.uint8), np.ascontiguousarray(b).view(np.uint8))
+NORMS = ["1", "2", "inf"]
+
+
+def oracle_bilevel(y32, eta, p="1", q="inf"):
+    return O.bilevel(np.asarray(y32, np.float64), eta, p, q)
+
+
+def run(y, eta, p="1", q="inf", flags=0):
+    x, budgets, z = mp.bilevel_project(y, eta, p, q, flags=flags)
+    return x, np.asarray(budgets), z
+
+
+# ---------------------------------------------------------------- goldens
+def test_golden_bilevel_f64(golden):
+    """f64 device path vs the compiled reference's own outputs."""
+    for i in range(int(golden["bi_count"][0])):
+        y = golden[f"bi{i}_y"].astype(np.float64)
+        p, q, eta = golden[f"bi{i}_meta"]
+        p, q = int(p), int(q)
+        x, b, z = run(y, eta, p, q)
+        xr, br = golden[f"bi{i}_x"], golden[f"bi{i}_b"]
+        np.testing.assert_allclose(b, br, rtol=1e-12, atol=1e-300, err_msg=f"case {i}")
+        np.testing.assert_allclose(x, xr, rtol=1e-12, atol=1e-15, err_msg=f"case {i}")
+        assert z == golden[f"bi{i}_z"][0], i
+
+
+def test_golden_bilevel_f32(golden):
+    """fp32 device path vs the reference (f64 on the same fp32 values)."""
+    for i in range(int(golden["bi_count"][0])):
+        y32 = golden[f"bi{i}_y"]
+        p, q, eta = golden[f"bi{i}_meta"]
+        qs = NORMS[int(q)]
+        x, b, z = run(y32, eta, int(p), int(q))
+        assert x.dtype == np.float32
+        ref = oracle_bilevel(y32, eta, NORMS[int(p)], qs)
+        assert bit_equal(ref["X"], golden[f"bi{i}_x"])
+        check_bilevel(x, y32, ref, qs, zero_cols_gpu=z)
+
+
+def test_golden_multilevel(golden):
+    for i in range(int(golden["ml_count"][0])):
+        t = golden[f"ml{i}_t"]
+        lv = [int(k) for k in golden[f"ml{i}_lv"]]
+        eta = float(golden[f"ml{i}_eta"][0])
+        x64, chain = mp.multilevel_project(t.astype(np.float64), lv, eta, return_chain=True)
+        np.testing.assert_allclose(x64, golden[f"ml{i}_x"], rtol=1e-12, atol=1e-15, err_msg=f"case {i}")
+        flat = np.concatenate([c.reshape(-1) for c in chain]) if chain else np.zeros(0)
+        np.testing.assert_allclose(flat, golden[f"ml{i}_chain"], rtol=1e-12, atol=1e-15, err_msg=f"case {i}")
+        x32 = mp.multilevel_project(t, lv, eta)
+        np.testing.assert_allclose(x32, golden[f"ml{i}_x"], rtol=2e-5, atol=1e-6, err_msg=f"case {i}")
+
+
+def test_golden_vector_balls(golden):
+    for i in range(int(golden["vb_count"][0])):
+        y = golden[f"vb{i}_y"].astype(np.float64)
+        q, r = golden[f"vb{i}_meta"]
+        x = mp.project_ball(y, int(q), r)
+        np.testing.assert_allclose(x, golden[f"vb{i}_x"], rtol=1e-12, atol=1e-15, err_msg=f"case {i}")
+
+
+# --------------------------------------------------- known answers (API)
+def test_reference_smoke_examples():  # proj/tests/python/test_smoke.py
+    np.testing.assert_allclose(mp.project_l1(np.array([1.0, 1.0]), 1.0), [0.5, 0.5], atol=1e-12)
+    np.testing.assert_allclose(mp.project_l2(np.array([3.0, 4.0]), 1.0), [0.6, 0.8], atol=1e-12)
+    np.testing.assert_allclose(mp.project_linf(np.array([0.7, -1.2]), 1.0), [0.7, -1.0])
+    x, budgets, z = mp.bilevel_project(np.eye(2), 1.0)
+    np.testing.assert_allclose(x, 0.5 * np.eye(2), atol=1e-12)
+    np.testing.assert_allclose(budgets, [0.5, 0.5], atol=1e-12)
+    assert z == 0
+    y = np.array([1.0, 0.2, 0.5, 0.4]).reshape(2, 1, 2)
+    x = mp.multilevel_project(y, "inf,inf,1", 1.0)
+    np.testing.assert_allclose(x, np.array([0.8, 0.2, 0.5, 0.2]).reshape(2, 1, 2), atol=1e-12)
+    assert mp.multilevel_norm(x, "inf,inf,1") <= 1.0 + 1e-9
+    assert mp.matrix_pq_norm(np.array([[1.0, 0.0], [1.0, 0.0]]), "1", "inf") == pytest.approx(1.0)
+    assert mp.structured_sparsity(np.array([[1.0, 0.0], [1.0, 0.0]]), 0.0) == (1, 0.5)
+    rng = np.random.default_rng(0)
+    y = rng.normal(size=(30, 20))
+    x, budgets, _ = mp.bilevel_project(y, 2.0)
+    assert mp.matrix_pq_norm(x, "1", "inf") <= 2.0 * (1 + 1e-9)
+    with pytest.raises(ValueError):
+        mp.project_l1(np.array([1.0]), -1.0)
+    with pytest.raises(ValueError):
+        mp.multilevel_project(np.eye(2), "inf,bogus", 1.0)
+
+
+def test_nonfinite_is_value_error():
+    y = np.ones((5, 7), np.float32)
+    for bad in (np.nan, np.inf, -np.inf):
+        for q in NORMS:
+            y2 = y.copy()
+            y2[3, 4] = bad
+            with pytest.raises(mp.MpValueError):
+                mp.bilevel_project(y2, 1.0, "1", q)
+    t = np.ones((3, 4, 5))
+    t[1, 2, 3] = np.nan
+    with pytest.raises(mp.MpValueError):
+        mp.multilevel_project(t, "inf,inf,1", 1.0)
+
+
+# ------------------------------------------------ configs (scaled, oracle)
+@pytest.mark.parametrize("p,q", [("1", "inf"), ("1", "1"), ("1", "2"), ("2", "inf"), ("inf", "inf"), ("2", "1")])
+@pytest.mark.parametrize("shape", [(1, 1), (1, 37), (37, 1), (129, 67), (300, 1001), (1000, 1000)])
+def test_bilevel_parity_shapes(p, q, shape):
+    y = datagen.normal(11, shape)
+    for rel in (0.0, 0.02, 0.3, 1.2):
+        eta = rel * O.matrix_pq_norm(y.astype(np.float64), p, q)
+        ref = oracle_bilevel(y, eta, p, q)
+        x, b, z = run(y, eta, p, q)
+        check_bilevel(x, y, ref, q, zero_cols_gpu=z)
+        if rel >= 1.2:
+            assert bit_equal(x, y)  # feasible input is the identity, bit for bit
+
+
+def test_config1_full():
+    y = datagen.config_input(1)
+    eta = 0.1 * O.matrix_pq_norm(y.astype(np.float64), "1", "inf")
+    ref = oracle_bilevel(y, eta)
+    x, b, z = run(y, eta)
+    rep = check_bilevel(x, y, ref, "inf", zero_cols_gpu=z)
+    assert z == ref["zero_columns"]
+    assert rep["max_rel"] < 1e-6
+
+
+@pytest.mark.parametrize("rel", [0.001, 0.01, 0.1, 0.5])
+def test_config2_full_radius_sweep(rel):
+    """Headline config: 10000 x 10000 U[-1,1], element-wise vs the oracle."""
+    y = datagen.config_input(2)
+    y64 = y.astype(np.float64)
+    eta = rel * O.matrix_pq_norm(y64, "1", "inf")
+    ref = O.bilevel(y64, eta)
+    del y64
+    x, b, z = run(y, eta)
+    check_bilevel(x, y, ref, "inf", zero_cols_gpu=z)
+    np.testing.assert_allclose(b, ref["budgets"], rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("q", ["1", "2"])
+def test_config3_full(q):
+    y = datagen.config_input(3)
+    y64 = y.astype(np.float64)
+    eta = 0.05 * O.matrix_pq_norm(y64, "1", q)
+    ref = O.bilevel(y64, eta, "1", q)
+    del y64
+    x, b, z = run(y, eta, "1", q)
+    check_bilevel(x, y, ref, q, zero_cols_gpu=z)
+
+
+def test_config4_full_trilevel():
+    t = datagen.config_input(4)
+    t64 = t.astype(np.float64)
+    eta = 0.05 * O.multilevel_norm(t64, ["inf", "inf", "1"])
+    xr = O.multilevel(t64, ["inf", "inf", "1"], eta)
+    x = mp.trilevel_project_l1infinf(t, eta)
+    assert x.dtype == np.float32
+    # tri-level == bi-level on the (d0*d1, d2) reshape
+    ref = O.bilevel(t64.reshape(256 * 256, 256), eta)
+    assert np.array_equal(ref["X"].reshape(t.shape), xr)
+    check_bilevel(x.reshape(256 * 256, 256), t.reshape(256 * 256, 256), ref, "inf")
+
+
+def test_config5_iteration0_full():
+    y = datagen.config_input(5)
+    v = np.abs(y).max(axis=0).astype(np.float64)
+    eta = datagen.config5_eta(v)
+    y64 = y.astype(np.float64)
+    ref = O.bilevel(y64, eta)
+    del y64
+    x, b, z = run(y, eta)
+    check_bilevel(x, y, ref, "inf", zero_cols_gpu=z)
+    assert ref["zero_columns"] == 7373 and z == 7373
+
+
+# --------------------------------------------------------- edge cases
+def test_ragged_and_unaligned():
+    rng = np.random.default_rng(3)
+    for n, m in [(5, 3), (7, 5), (64, 6), (33, 1023), (2, 4097)]:
+        y = rng.normal(size=(n, m)).astype(np.float32)
+        for q in NORMS:
+            eta = 0.2 * O.matrix_pq_norm(y.astype(np.float64), "1", q)
+            x, b, z = run(y, eta, "1", q)
+            check_bilevel(x, y, oracle_bilevel(y, eta, "1", q), q, zero_cols_gpu=z)
+
+
+def test_large_m_cooperative_outer():
+    """m > 24576: the outer l1 projection runs as a cooperative grid."""
+    y = datagen.normal(12, (3, 70000))
+    for q in NORMS:
+        eta = 0.05 * O.matrix_pq_norm(y.astype(np.float64), "1", q)
+        x, b, z = run(y, eta, "1", q)
+        check_bilevel(x, y, oracle_bilevel(y, eta, "1", q), q, zero_cols_gpu=z)
+    v = datagen.normal(13, (300001,)).astype(np.float64)
+    for q in NORMS:
+        r = 0.1 * O.multilevel_norm(v, [q])
+        np.testing.assert_allclose(mp.project_ball(v, q, r), O.project_ball(v, q, r), rtol=1e-10, atol=1e-13)
+
+
+def test_l11_unstaged_tall_columns():
+    """n beyond the cluster's shared-memory capacity: unstaged strip path."""
+    y = datagen.normal(14, (60000, 40))
+    eta = 0.05 * O.matrix_pq_norm(y.astype(np.float64), "1", "1")
+    x, b, z = run(y, eta, "1", "1")
+    check_bilevel(x, y, oracle_bilevel(y, eta, "1", "1"), "1", zero_cols_gpu=z)
+
+
+def test_eta_zero_and_zero_sign():
+    y = datagen.normal(15, (50, 40))
+    x, b, z = run(y, 0.0)
+    assert z == 40 and np.all(x == 0)
+    # default: zero-budget columns written as +0 without a read
+    assert not np.any(np.signbit(x))
+    # exact flag: copysign(0, y) bytes like proj/src/fiber_kernels.cpp:47
+    x2, _, _ = run(y, 0.0, flags=mp.MP_FLAG_EXACT_ZERO_SIGN)
+    ref = oracle_bilevel(y, 0.0)
+    assert bit_equal(x2, ref["X"].astype(np.float32))
+
+
+def test_exact_flag_bitwise_vs_rounded_reference():
+    """With exact zero signs, l_{1,inf} output equals RN(reference) bit for
+    bit except in the near-threshold band (compare uses RD(u), value RN(u))."""
+    y = datagen.uniform(16, (400, 333), -1.0, 1.0)
+    eta = 0.05 * O.matrix_pq_norm(y.astype(np.float64), "1", "inf")
+    ref = oracle_bilevel(y, eta)
+    x, _, _ = run(y, eta, flags=mp.MP_FLAG_EXACT_ZERO_SIGN)
+    near = np.abs(ref["v"] - ref["tau"]) <= 1e-5 * ref["tau"]
+    same = np.all(x.view(np.uint32) == ref["X"].astype(np.float32).view(np.uint32), axis=0)
+    assert np.all(same | near)
+
+
+# ------------------------------------------------------ device API / graphs
+def test_device_api_graph_determinism_inplace():
+    import torch
+    y = torch.from_numpy(datagen.uniform(17, (2000, 3000), -1.0, 1.0)).cuda()
+    eta = 0.01 * float(y.abs().amax(dim=0).double().sum())
+    proj = mp.BilevelProjector(2000, 3000, "float32", "1", "inf")
+    x1 = torch.empty_like(y)
+    proj(y, x1, eta)
+    torch.cuda.synchronize()
+    x2 = torch.empty_like(y)
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            proj(y, x2, eta, stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(x1.view(torch.int32), x2.view(torch.int32))
+    y3 = y.clone()
+    proj(y3, y3, eta)  # in place
+    torch.cuda.synchronize()
+    assert torch.equal(x1.view(torch.int32), y3.view(torch.int32))
+    for q in ("1", "2"):
+        pq = mp.BilevelProjector(2000, 3000, "float32", "1", q)
+        a, b = torch.empty_like(y), torch.empty_like(y)
+        pq(y, a, eta * 50)
+        pq(y, b, eta * 50)
+        torch.cuda.synchronize()
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32))  # run-to-run bitwise
+
+
+def test_idempotence_full_size():
+    """Project, then project the result at eta(1+1e-6): identical bytes."""
+    y = datagen.config_input(2, scale=0.5)
+    eta = 0.01 * O.matrix_pq_norm(y.astype(np.float64), "1", "inf")
+    x, _, _ = run(y, eta)
+    x2, _, _ = run(x, eta * (1 + 1e-6))
+    assert bit_equal(x, x2)
+    colmax = np.abs(x.astype(np.float64)).max(axis=0)
+    assert colmax.sum() <= eta * (1 + 1e-6)
