@@ -164,6 +164,12 @@ mp_status mp_aggregate_host(mp_context* ctx, const void* t, double* out, mp_dtyp
  * NULL / 0 to disable. */
 void mp_profile_events(void* const* events, int count);
 
+/* Device-side timeline (profiling aid): while set (device pointer to 8
+ * uint64, caller-initialised to {UINT64_MAX, 0} pairs), kernels fold their
+ * %globaltimer start (min) / end (max) into [2k], [2k+1] for k = 0 norm pass,
+ * 1 norm finalize, 2 outer projection, 3 apply pass.  NULL disables. */
+void mp_profile_timeline(unsigned long long* device_buf);
+
 /* Thread-local description of the last non-OK status. */
 const char* mp_last_error(void);
 

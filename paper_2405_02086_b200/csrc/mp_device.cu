@@ -63,105 +63,233 @@ struct Grid {
   int64_t rpb = 1;     // rows per block
 };
 
-Grid plan_grid(int vec, int64_t n, int64_t m) {
+// Balanced column tiles: the fewest tiles of <= 256 threads, all the same
+// width (m = 10000, VEC = 4: 10 tiles of 250 threads), so no CTA is short.
+int threads_for(int vec, int64_t m) {
+  const int64_t slots = (m + vec - 1) / vec;
+  const int64_t tiles = (slots + mpk::kThreads - 1) / mpk::kThreads;
+  return static_cast<int>((slots + tiles - 1) / tiles);
+}
+
+// Launch with programmatic stream serialization (PDL): the kernel may be
+// scheduled while its predecessor drains and synchronises with
+// griddepcontrol.wait before touching the predecessor's outputs.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, static_cast<KArgs>(args)...);
+}
+
+// One resident wave: grid.y = floor(SMs * occupancy / column tiles) row
+// blocks, so every CTA starts at once and none trails in a second wave (a
+// 1.005-wave grid costs a whole extra CTA lifetime).  Each thread keeps U
+// 16-byte loads in flight; at full occupancy that is >= 128 KiB per SM, well
+// above the ~35 KiB Little's law asks of HBM3e.
+Grid plan_grid(int vec, int64_t n, int64_t m, int ctas_per_sm) {
   Grid g;
   g.vec = vec;
+  g.threads = threads_for(vec, m);
   const int64_t slots = (m + vec - 1) / vec;
-  g.threads = static_cast<int>(std::min<int64_t>(mpk::kThreads, ((slots + 31) / 32) * 32));
   g.ntiles = (slots + g.threads - 1) / g.threads;
-  // ~2048 resident threads per SM: enough 16-byte loads in flight to cover
-  // HBM latency (U loads per thread), grid a whole multiple of the SM count.
-  const int64_t target_ctas = static_cast<int64_t>(sm_count()) * (2048 / g.threads);
-  int64_t nrb = (target_ctas + g.ntiles - 1) / g.ntiles;
-  nrb = std::max<int64_t>(1, std::min<int64_t>(nrb, (n + 3) / 4));
+  const int64_t resident = static_cast<int64_t>(sm_count()) * std::max(1, ctas_per_sm);
+  int64_t nrb = std::max<int64_t>(1, resident / g.ntiles);
+  nrb = std::min<int64_t>(nrb, std::max<int64_t>(1, (n + 3) / 4));  // >= 4 rows per block
   nrb = std::min<int64_t>(nrb, 65535);
   g.rpb = (n + nrb - 1) / nrb;
   g.nrb = (n + g.rpb - 1) / g.rpb;
   return g;
 }
 
+
+// Occupancy of one kernel instantiation (cached per function and block size).
+int occupancy(const void* fn, int threads) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, int>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : cache)
+    if (e.first.first == fn && e.first.second == threads) return e.second;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, 0) != cudaSuccess || occ < 1) occ = 1;
+  cache.push_back({{fn, threads}, occ});
+  return occ;
+}
+
 int pick_vec(mp_dtype dt, int64_t m, const void* a, const void* b) {
   const uintptr_t al = reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b);
+  // 32-byte packs (256-bit LDG/STG on sm_100) when rows stay 32-byte aligned
   if (dt == MP_F32) {
+    if (m % 8 == 0 && al % 32 == 0) return 8;
     if (m % 4 == 0 && al % 16 == 0) return 4;
     if (m % 2 == 0 && al % 8 == 0) return 2;
     return 1;
   }
+  if (m % 4 == 0 && al % 32 == 0) return 4;
   if (m % 2 == 0 && al % 16 == 0) return 2;
   return 1;
 }
 
-// Largest row-block count over every vector width the plan may pick.
+// Upper bound of the K1 row-block count over every vector width and any
+// occupancy (sizes the l1/l2 partials in the workspace).
 int64_t max_nrb(mp_dtype dt, int64_t n, int64_t m) {
   int64_t r = 1;
-  for (int v : {1, 2, 4}) {
-    if (dt == MP_F64 && v == 4) continue;
-    r = std::max(r, plan_grid(v, n, m).nrb);
+  for (int v : {1, 2, 4, 8}) {
+    if (dt == MP_F64 && v == 8) continue;
+    const int t = threads_for(v, m);
+    r = std::max(r, plan_grid(v, n, m, std::min(32, 2048 / t)).nrb);
   }
   return r;
 }
 
 // --------------------------------------------------------------- dispatch
-template <typename T, int VEC>
-cudaError_t launch_colnorm_v(int q, const Grid& g, const T* y, int64_t n, int64_t m, void* out, cudaStream_t s) {
+// K1 and K3 of one projection share the row partition (the smaller of their
+// two occupancies), so every K3 CTA starts on exactly the rows its K1
+// counterpart read last -- still resident in L2.
+template <typename T, int VEC, int Q>
+int pair_occupancy(int threads) {
+  constexpr int QA = (Q == mpk::kL2) ? mpk::kL2 : mpk::kInf;
+  constexpr int U1 = (sizeof(T) * VEC == 32) ? 4 : 8;
+  const int o1 = occupancy(reinterpret_cast<const void*>(mpk::k_colnorm<T, VEC, Q, U1>), threads);
+  const int o3 = occupancy(reinterpret_cast<const void*>(mpk::k_apply<T, VEC, QA, 4, true>), threads);
+  return std::min(o1, o3);
+}
+
+template <typename T, int VEC, int Q>
+cudaError_t launch_colnorm_q(int64_t n, int64_t m, const T* y, void* out, Grid& g, cudaStream_t s) {
+  constexpr int U = (sizeof(T) * VEC == 32) ? 4 : 8;  // 128 bytes of loads in flight per thread
+  auto fn = mpk::k_colnorm<T, VEC, Q, U>;
+  const int t = threads_for(VEC, m);
+  g = plan_grid(VEC, n, m, pair_occupancy<T, VEC, Q>(t));
   dim3 grid(static_cast<unsigned>(g.ntiles), static_cast<unsigned>(g.nrb));
-  constexpr int U = 8;
-  if (q == mpk::kInf) mpk::k_colnorm<T, VEC, mpk::kInf, U><<<grid, g.threads, 0, s>>>(y, n, m, g.rpb, out);
-  else if (q == mpk::kL1) mpk::k_colnorm<T, VEC, mpk::kL1, U><<<grid, g.threads, 0, s>>>(y, n, m, g.rpb, out);
-  else mpk::k_colnorm<T, VEC, mpk::kL2, U><<<grid, g.threads, 0, s>>>(y, n, m, g.rpb, out);
+  fn<<<grid, g.threads, 0, s>>>(y, n, m, g.rpb, out);
   return cudaGetLastError();
 }
 
-template <typename T>
-cudaError_t launch_colnorm(int q, const Grid& g, const T* y, int64_t n, int64_t m, void* out, cudaStream_t s) {
-  if (g.vec == 4) {
-    if constexpr (sizeof(T) == 4) return launch_colnorm_v<T, 4>(q, g, y, n, m, out, s);
-  }
-  if (g.vec == 2) return launch_colnorm_v<T, 2>(q, g, y, n, m, out, s);
-  return launch_colnorm_v<T, 1>(q, g, y, n, m, out, s);
+template <typename T, int VEC>
+cudaError_t launch_colnorm_v(int q, const T* y, int64_t n, int64_t m, void* out, Grid& g, cudaStream_t s) {
+  if (q == mpk::kInf) return launch_colnorm_q<T, VEC, mpk::kInf>(n, m, y, out, g, s);
+  if (q == mpk::kL1) return launch_colnorm_q<T, VEC, mpk::kL1>(n, m, y, out, g, s);
+  return launch_colnorm_q<T, VEC, mpk::kL2>(n, m, y, out, g, s);
 }
 
-template <typename T, int VEC>
-cudaError_t launch_apply_v(int q, const Grid& g, const T* y, T* x, int64_t n, int64_t m, const void* colp,
-                           const double* budgets, const mp_info* info, unsigned flags, cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>(g.ntiles), static_cast<unsigned>(g.nrb));
+// K1; `g` returns the grid used (g.nrb = number of l1/l2 partial rows).
+template <typename T>
+cudaError_t launch_colnorm(int q, int vec, const T* y, int64_t n, int64_t m, void* out, Grid& g, cudaStream_t s) {
+  if (vec == 8) {
+    if constexpr (sizeof(T) == 4) return launch_colnorm_v<T, 8>(q, y, n, m, out, g, s);
+  }
+  if (vec == 4) return launch_colnorm_v<T, 4>(q, y, n, m, out, g, s);
+  if (vec == 2) return launch_colnorm_v<T, 2>(q, y, n, m, out, g, s);
+  return launch_colnorm_v<T, 1>(q, y, n, m, out, g, s);
+}
+
+template <typename T, int VEC, int Q>
+cudaError_t launch_apply_q(const T* y, T* x, int64_t n, int64_t m, const mpk::ApplyCols& A, bool derive,
+                           const mp_info* info, unsigned flags, cudaStream_t s) {
   constexpr int U = 4;
-  if (q == mpk::kInf)
-    mpk::k_apply<T, VEC, mpk::kInf, U><<<grid, g.threads, 0, s>>>(y, x, n, m, g.rpb, static_cast<int>(g.nrb), colp,
-                                                                   budgets, info, flags);
-  else
-    mpk::k_apply<T, VEC, mpk::kL2, U><<<grid, g.threads, 0, s>>>(y, x, n, m, g.rpb, static_cast<int>(g.nrb), colp,
-                                                                  budgets, info, flags);
-  return cudaGetLastError();
+  const int t = threads_for(VEC, m);
+  const Grid g = plan_grid(VEC, n, m, pair_occupancy<T, VEC, Q>(t));
+  dim3 grid(static_cast<unsigned>(g.ntiles), static_cast<unsigned>(g.nrb));
+  if (derive)
+    return launch_pdl(mpk::k_apply<T, VEC, Q, U, true>, grid, dim3(g.threads), 0, s, y, x, n, m, g.rpb, A, info,
+                      flags);
+  return launch_pdl(mpk::k_apply<T, VEC, Q, U, false>, grid, dim3(g.threads), 0, s, y, x, n, m, g.rpb, A, info,
+                    flags);
+}
+
+template <typename T, int VEC>
+cudaError_t launch_apply_v(int q, const T* y, T* x, int64_t n, int64_t m, const mpk::ApplyCols& A, bool derive,
+                           const mp_info* info, unsigned flags, cudaStream_t s) {
+  if (q == mpk::kInf) return launch_apply_q<T, VEC, mpk::kInf>(y, x, n, m, A, derive, info, flags, s);
+  return launch_apply_q<T, VEC, mpk::kL2>(y, x, n, m, A, derive, info, flags, s);
 }
 
 template <typename T>
-cudaError_t launch_apply(int q, const Grid& g, const T* y, T* x, int64_t n, int64_t m, const void* colp,
-                         const double* budgets, const mp_info* info, unsigned flags, cudaStream_t s) {
-  if (g.vec == 4) {
-    if constexpr (sizeof(T) == 4) return launch_apply_v<T, 4>(q, g, y, x, n, m, colp, budgets, info, flags, s);
+cudaError_t launch_apply(int q, int vec, const T* y, T* x, int64_t n, int64_t m, const mpk::ApplyCols& A,
+                         bool derive, const mp_info* info, unsigned flags, cudaStream_t s) {
+  if (vec == 8) {
+    if constexpr (sizeof(T) == 4) return launch_apply_v<T, 8>(q, y, x, n, m, A, derive, info, flags, s);
   }
-  if (g.vec == 2) return launch_apply_v<T, 2>(q, g, y, x, n, m, colp, budgets, info, flags, s);
-  return launch_apply_v<T, 1>(q, g, y, x, n, m, colp, budgets, info, flags, s);
+  if (vec == 4) return launch_apply_v<T, 4>(q, y, x, n, m, A, derive, info, flags, s);
+  if (vec == 2) return launch_apply_v<T, 2>(q, y, x, n, m, A, derive, info, flags, s);
+  return launch_apply_v<T, 1>(q, y, x, n, m, A, derive, info, flags, s);
+}
+
+template <int P>
+cudaError_t outer_attr() {
+  cudaError_t e = cudaFuncSetAttribute(mpk::k_outer<P>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(mpk::k_outer<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(P * mpk::kOuterThreads * sizeof(double)));
 }
 
 cudaError_t outer_setup() {
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    err = cudaFuncSetAttribute(mpk::k_outer, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(mpk::kOuterMaxM * sizeof(double)));
-    if (err == cudaSuccess) err = mpk::l1strip_setup();
+    for (cudaError_t e : {outer_attr<1>(), outer_attr<2>(), outer_attr<4>(), outer_attr<8>(), outer_attr<12>(),
+                          outer_attr<16>(), outer_attr<24>(), mpk::l1strip_setup()})
+      if (e != cudaSuccess && err == cudaSuccess) err = e;
   });
   return err;
+}
+
+// K2 on a cluster of C CTAs (PDL + cluster launch attributes).
+template <int P>
+cudaError_t launch_outer_p(const mpk::OuterArgs& a, int C, int chunk, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(mpk::kOuterThreads);
+  cfg.dynamicSmemBytes = static_cast<size_t>(std::max(chunk, 1)) * sizeof(double);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = C;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, mpk::k_outer<P>, a);
+}
+
+template <int P>
+cudaError_t launch_outer_reg(const mpk::OuterArgs& a, cudaStream_t s) {
+  return launch_pdl(mpk::k_outer_reg<P>, dim3(1), dim3(mpk::kOuterRegThreads), 0, s, a);
 }
 
 cudaError_t launch_outer(const mpk::OuterArgs& a, cudaStream_t s) {
   cudaError_t e = outer_setup();
   if (e != cudaSuccess) return e;
-  const size_t smem = static_cast<size_t>(std::max<int64_t>(a.m, 1)) * sizeof(double);
-  mpk::k_outer<<<1, mpk::kOuterThreads, smem, s>>>(a);
-  return cudaGetLastError();
+  if (a.m <= mpk::kOuterRegMaxM) {
+    const int64_t per = (std::max<int64_t>(a.m, 1) + mpk::kOuterRegThreads - 1) / mpk::kOuterRegThreads;
+    if (per <= 1) return launch_outer_reg<1>(a, s);
+    if (per <= 2) return launch_outer_reg<2>(a, s);
+    if (per <= 4) return launch_outer_reg<4>(a, s);
+    if (per <= 8) return launch_outer_reg<8>(a, s);
+    return launch_outer_reg<12>(a, s);
+  }
+  // ~2048 elements (8 per thread) per CTA, at most 16 CTAs per cluster.
+  const int64_t m = std::max<int64_t>(a.m, 1);
+  const int C = static_cast<int>(std::min<int64_t>(mpk::kOuterMaxCluster, (m + 2047) / 2048));
+  const int chunk = static_cast<int>((m + C - 1) / C);
+  const int per = (chunk + mpk::kOuterThreads - 1) / mpk::kOuterThreads;
+  if (per <= 1) return launch_outer_p<1>(a, C, chunk, s);
+  if (per <= 2) return launch_outer_p<2>(a, C, chunk, s);
+  if (per <= 4) return launch_outer_p<4>(a, C, chunk, s);
+  if (per <= 8) return launch_outer_p<8>(a, C, chunk, s);
+  if (per <= 12) return launch_outer_p<12>(a, C, chunk, s);
+  if (per <= 16) return launch_outer_p<16>(a, C, chunk, s);
+  return launch_outer_p<24>(a, C, chunk, s);
 }
 
 // Column parameters for a fiber projection from (norms v, budgets u).
@@ -191,6 +319,7 @@ struct BilevelWs {
   void* colp;        // per-column apply parameters
   mpk::L1StripWs l1; // l1 inner projection scratch
   void* large;       // k_outer_large scratch (m > kOuterMaxM)
+  mpk::OuterParams* params;  // K2 -> apply: mode / tau / scale
 };
 
 BilevelWs carve_bilevel(Carve& c, mp_dtype dt, int64_t n, int64_t m, mp_norm q) {
@@ -203,6 +332,7 @@ BilevelWs carve_bilevel(Carve& c, mp_dtype dt, int64_t n, int64_t m, mp_norm q) 
   w.colp = c.take<double>(m);
   if (q == MP_NORM_L1) w.l1 = mpk::carve_l1strip(c, m);
   w.large = c.take<char>(mpk::outer_large_ws_bytes(m));
+  w.params = c.take<mpk::OuterParams>(1);
   return w;
 }
 
@@ -213,10 +343,27 @@ cudaError_t project_fibers(const T* y, T* x, int64_t n, int64_t m, int q, const 
                            const void* colp, const mpk::L1StripWs& l1, const mp_info* info, unsigned flags,
                            mp_dtype dt, cudaStream_t s) {
   if (q == mpk::kL1) return mpk::launch_l1strip<T>(y, x, n, m, v, u, l1, info, flags, s);
-  Grid g = plan_grid(pick_vec(dt, m, y, x), n, m);
-  return launch_apply<T>(q, g, y, x, n, m, colp, u, info, flags, s);
+  mpk::ApplyCols A{};
+  A.colp = colp;
+  A.budgets = u;
+  return launch_apply<T>(q, pick_vec(dt, m, y, x), y, x, n, m, A, false, info, flags, s);
 }
 
+// K1 partials (l1 / l2) -> norms.
+cudaError_t launch_norm_reduce(int q, const void* part, int64_t R, int64_t m, double* v, cudaStream_t s) {
+  const unsigned blocks = static_cast<unsigned>((m + 31) / 32);
+  if (q == mpk::kL1)
+    return launch_pdl(mpk::k_colnorm_reduce<mpk::kL1>, dim3(blocks), dim3(256), 0, s, static_cast<const double*>(part),
+                      R, m, v);
+  return launch_pdl(mpk::k_colnorm_reduce<mpk::kL2>, dim3(blocks), dim3(256), 0, s, static_cast<const double*>(part),
+                    R, m, v);
+}
+
+// The bi-level hot path (proj/src/bilevel.cpp:10-32):
+//   [memset] K1 norms -> (l1/l2: reduce partials) -> K2 outer threshold ->
+//   K3 apply, each later kernel PDL-chained to its producer.  K2 publishes
+//   only (mode, tau, scale); K3 / the l1 strips derive every budget from its
+//   norm, write the user-facing budgets and count zero columns.
 template <typename T>
 mp_status bilevel_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, mp_norm p, mp_norm q, double eta,
                        double* budgets, double* norms, mp_info* info, unsigned flags, void* ws, size_t wsb,
@@ -224,11 +371,15 @@ mp_status bilevel_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, mp_n
   Carve c(ws, wsb);
   BilevelWs w = carve_bilevel(c, dt, n, m, q);
   if (!c.fits()) return fail(MP_ERR_WORKSPACE, "mp_bilevel_project: workspace too small");
+  MP_CUDA_TRY(outer_setup());
   mp_info* inf = info ? info : w.info;
   double* u = budgets ? budgets : w.budgets;
   double* v = norms ? norms : w.v;
+  // The huge-n l1 fallback reads materialised budgets; everything else derives.
+  const bool derive = !(q == MP_NORM_L1 && !mpk::l1_staged_ok<T>(n));
 
-  const Grid g = plan_grid(pick_vec(dt, m, y, x), n, m);
+  const int vec = pick_vec(dt, m, y, x);
+  Grid g;
   prof_mark(0, s);
   mpk::OuterArgs oa{};
   oa.m = m;
@@ -237,26 +388,27 @@ mp_status bilevel_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, mp_n
   oa.u_out = u;
   oa.info = inf;
   oa.scratch = w.large;
+  oa.params = w.params;
+  oa.emit = derive ? 0 : 1;
+  mpk::ApplyCols A{};
+  A.params = w.params;
+  A.u_out = u;
+  A.info_w = inf;
   if (q == MP_NORM_INF) {
     MP_CUDA_TRY(cudaMemsetAsync(w.k1out, 0, static_cast<size_t>(m) * sizeof(unsigned long long), s));
-    MP_CUDA_TRY(launch_colnorm<T>(q, g, y, n, m, w.k1out, s));
+    MP_CUDA_TRY(launch_colnorm<T>(q, vec, y, n, m, w.k1out, g, s));
     oa.vin = w.k1out;
     oa.vkind = sizeof(T) == 4 ? 0 : 1;  // f64 |y| bits are the f64 values
-    oa.v_out = (norms || sizeof(T) == 8) ? v : nullptr;
-    if constexpr (sizeof(T) == 4) oa.rdrn = static_cast<float2*>(w.colp);
-    else oa.v_out = v;  // the apply reads budgets directly; keep v for symmetry
+    A.v = w.k1out;
+    A.vkind = oa.vkind;
+    A.v_out = norms;
   } else {
-    MP_CUDA_TRY(launch_colnorm<T>(q, g, y, n, m, w.k1out, s));
-    const int fin_threads = 256;
-    const unsigned fin_blocks = static_cast<unsigned>((m + fin_threads - 1) / fin_threads);
-    if (q == MP_NORM_L1)
-      mpk::k_colnorm_finalize<mpk::kL1><<<fin_blocks, fin_threads, 0, s>>>(w.k1out, g.nrb, m, 0, v);
-    else
-      mpk::k_colnorm_finalize<mpk::kL2><<<fin_blocks, fin_threads, 0, s>>>(w.k1out, g.nrb, m, 0, v);
-    MP_CUDA_TRY(cudaGetLastError());
+    MP_CUDA_TRY(launch_colnorm<T>(q, vec, y, n, m, w.k1out, g, s));
+    MP_CUDA_TRY(launch_norm_reduce(q, w.k1out, g.nrb, m, v, s));
     oa.vin = v;
     oa.vkind = 1;
-    if (q == MP_NORM_L2) oa.factor = static_cast<double*>(w.colp);
+    A.v = v;
+    A.vkind = 1;
   }
   prof_mark(1, s);
   if (m > mpk::kOuterMaxM) {
@@ -265,8 +417,17 @@ mp_status bilevel_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, mp_n
     MP_CUDA_TRY(launch_outer(oa, s));
   }
   prof_mark(2, s);
-  const void* colp = (q == MP_NORM_INF && sizeof(T) == 8) ? static_cast<const void*>(u) : w.colp;
-  MP_CUDA_TRY(project_fibers<T>(y, x, n, m, q, v, u, colp, w.l1, inf, flags, dt, s));
+  if (q == MP_NORM_L1) {
+    mpk::L1Derive dv;
+    if (derive) {
+      dv.params = w.params;
+      dv.u_out = u;
+      dv.info_w = inf;
+    }
+    MP_CUDA_TRY(mpk::launch_l1strip<T>(y, x, n, m, v, u, w.l1, inf, flags, s, dv));
+  } else {
+    MP_CUDA_TRY(launch_apply<T>(q, vec, y, x, n, m, A, true, inf, flags, s));
+  }
   prof_mark(3, s);
   return MP_OK;
 }
@@ -318,6 +479,7 @@ mp_status vector_impl(const void* y, void* x, mp_dtype dt, int64_t len, mp_norm 
   oa.u_out = dt == MP_F32 ? w.u : static_cast<double*>(x);
   oa.info = inf;
   oa.scratch = w.large;
+  oa.emit = 1;
   if (len > mpk::kOuterMaxM) {
     MP_CUDA_TRY(mpk::launch_outer_large(oa, s));
   } else {
@@ -337,17 +499,17 @@ mp_status vector_impl(const void* y, void* x, mp_dtype dt, int64_t len, mp_norm 
 template <typename T>
 mp_status aggregate_impl(const T* t, double* out, mp_dtype dt, int64_t n, int64_t m, int q, void* scratch,
                          cudaStream_t s) {
-  const Grid g = plan_grid(pick_vec(dt, m, t, t), n, m);
+  const int vec = pick_vec(dt, m, t, t);
+  Grid g;
   const unsigned fin_blocks = static_cast<unsigned>((m + 255) / 256);
   if (q == mpk::kInf) {
     void* bits = sizeof(T) == 8 ? static_cast<void*>(out) : scratch;
     MP_CUDA_TRY(cudaMemsetAsync(bits, 0, static_cast<size_t>(m) * sizeof(T), s));
-    MP_CUDA_TRY(launch_colnorm<T>(q, g, t, n, m, bits, s));
+    MP_CUDA_TRY(launch_colnorm<T>(q, vec, t, n, m, bits, g, s));
     if (sizeof(T) == 4) mpk::k_colnorm_finalize<mpk::kInf><<<fin_blocks, 256, 0, s>>>(bits, 1, m, 0, out);
   } else {
-    MP_CUDA_TRY(launch_colnorm<T>(q, g, t, n, m, scratch, s));
-    if (q == mpk::kL1) mpk::k_colnorm_finalize<mpk::kL1><<<fin_blocks, 256, 0, s>>>(scratch, g.nrb, m, 0, out);
-    else mpk::k_colnorm_finalize<mpk::kL2><<<fin_blocks, 256, 0, s>>>(scratch, g.nrb, m, 0, out);
+    MP_CUDA_TRY(launch_colnorm<T>(q, vec, t, n, m, scratch, g, s));
+    MP_CUDA_TRY(launch_norm_reduce(q, scratch, g.nrb, m, out, s));
   }
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
@@ -412,6 +574,7 @@ mp_status multilevel_impl(const T* t, T* x, mp_dtype dt, const int64_t* shape, i
   Carve c(ws, wsb);
   MultiWs w = carve_multi(c, dt, shape, order, levels);
   if (!c.fits()) return fail(MP_ERR_WORKSPACE, "mp_multilevel_project: workspace too small");
+  MP_CUDA_TRY(outer_setup());
   if (order == 1) return vector_impl(t, x, dt, shape[0], levels[0], eta, info, w.vec, s);
 
   std::vector<int64_t> M(order + 1, 1);
@@ -443,6 +606,7 @@ mp_status multilevel_impl(const T* t, T* x, mp_dtype dt, const int64_t* shape, i
   oa.u_out = B[order - 1];
   oa.info = inf;
   oa.scratch = w.large;
+  oa.emit = 1;
   if (oa.m > mpk::kOuterMaxM) {
     MP_CUDA_TRY(mpk::launch_outer_large(oa, s));
   } else {
@@ -480,6 +644,10 @@ mp_status check_multi_args(const void* t, const void* x, mp_dtype dt, const int6
 extern "C" {
 
 const char* mp_last_error(void) { return last_error(); }
+
+void mp_profile_timeline(unsigned long long* device_buf) {
+  cudaMemcpyToSymbol(mpk::g_mp_timeline, &device_buf, sizeof(device_buf));
+}
 
 void mp_profile_events(void* const* events, int count) {
   for (int i = 0; i < 4; ++i)

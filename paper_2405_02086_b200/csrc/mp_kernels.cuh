@@ -20,6 +20,7 @@
 //                      so the L2-resident tail of K1 is re-used.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -27,15 +28,20 @@
 
 namespace mpk {
 
+namespace cg = cooperative_groups;
+
 constexpr int kL1 = 0, kL2 = 1, kInf = 2;
 constexpr int kThreads = 256;  // K1 / K3 CTA size
-constexpr int kOuterThreads = 1024;
+constexpr int kOuterThreads = 256;   // K2 threads per cluster CTA
+constexpr int kOuterMaxCluster = 16;
 
 // ------------------------------------------------------------ pack helpers
 template <typename T, int VEC> struct PackT;
+template <> struct PackT<float, 8> { using type = float4; };  // 256-bit path uses inline PTX
 template <> struct PackT<float, 4> { using type = float4; };
 template <> struct PackT<float, 2> { using type = float2; };
 template <> struct PackT<float, 1> { using type = float; };
+template <> struct PackT<double, 4> { using type = double2; };  // 256-bit path uses inline PTX
 template <> struct PackT<double, 2> { using type = double2; };
 template <> struct PackT<double, 1> { using type = double; };
 
@@ -53,24 +59,84 @@ __device__ __forceinline__ unsigned long long abs_bits(double v) {
 // Read-only path; K1 keeps lines in L2 (default policy) so K3 can reuse them.
 template <typename T, int VEC>
 __device__ __forceinline__ void load_keep(const T* p, T (&o)[VEC]) {
-  using V = typename PackT<T, VEC>::type;
-  V v = __ldg(reinterpret_cast<const V*>(p));
-  memcpy(o, &v, sizeof(V));
+  if constexpr (sizeof(T) * VEC == 32) {
+    // 256-bit LDG (sm_100): half the LSU instructions of float4 loads
+    if constexpr (sizeof(T) == 4)
+      asm("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+          : "=f"(o[0]), "=f"(o[1]), "=f"(o[2]), "=f"(o[3]), "=f"(o[4]), "=f"(o[5]), "=f"(o[6]), "=f"(o[7])
+          : "l"(p));
+    else
+      asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+          : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3])
+          : "l"(p));
+  } else {
+    using V = typename PackT<T, VEC>::type;
+    V v = __ldg(reinterpret_cast<const V*>(p));
+    memcpy(o, &v, sizeof(V));
+  }
 }
 // Last use of the data: evict-first.
 template <typename T, int VEC>
 __device__ __forceinline__ void load_last(const T* p, T (&o)[VEC]) {
-  using V = typename PackT<T, VEC>::type;
-  V v = __ldcs(reinterpret_cast<const V*>(p));
-  memcpy(o, &v, sizeof(V));
+  if constexpr (sizeof(T) * VEC == 32) {
+    if constexpr (sizeof(T) == 4)
+      asm("ld.global.cs.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+          : "=f"(o[0]), "=f"(o[1]), "=f"(o[2]), "=f"(o[3]), "=f"(o[4]), "=f"(o[5]), "=f"(o[6]), "=f"(o[7])
+          : "l"(p));
+    else
+      asm("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3]) : "l"(p));
+  } else {
+    using V = typename PackT<T, VEC>::type;
+    V v = __ldcs(reinterpret_cast<const V*>(p));
+    memcpy(o, &v, sizeof(V));
+  }
 }
 template <typename T, int VEC>
 __device__ __forceinline__ void store_stream(T* p, const T (&o)[VEC]) {
-  using V = typename PackT<T, VEC>::type;
-  V v;
-  memcpy(&v, o, sizeof(V));
-  __stcs(reinterpret_cast<V*>(p), v);
+  if constexpr (sizeof(T) * VEC == 32) {
+    if constexpr (sizeof(T) == 4)
+      asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(o[0]), "f"(o[1]), "f"(o[2]),
+                   "f"(o[3]), "f"(o[4]), "f"(o[5]), "f"(o[6]), "f"(o[7])
+                   : "memory");
+    else
+      asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(o[0]), "d"(o[1]), "d"(o[2]), "d"(o[3])
+                   : "memory");
+  } else {
+    using V = typename PackT<T, VEC>::type;
+    V v;
+    memcpy(&v, o, sizeof(V));
+    __stcs(reinterpret_cast<V*>(p), v);
+  }
 }
+
+// Device-side timeline (profiling aid, mp_profile_timeline): when set, thread
+// 0 of every CTA folds %globaltimer into [2k] = min start, [2k+1] = max end
+// for kernel k (0 K1, 1 finalize, 2 K2, 3 K3).  One predicated load per CTA
+// when unset.
+__device__ unsigned long long* g_mp_timeline = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void tl_begin(int k) {
+  if (threadIdx.x == 0) {
+    unsigned long long* tl = g_mp_timeline;
+    if (tl) atomicMin(tl + 2 * k, gtimer());
+  }
+}
+__device__ __forceinline__ void tl_end(int k) {
+  if (threadIdx.x == 0) {
+    unsigned long long* tl = g_mp_timeline;
+    if (tl) atomicMax(tl + 2 * k + 1, gtimer());
+  }
+}
+
+// Programmatic dependent launch (sm_90+): wait for the producer grid's
+// memory, and let the consumer grid be scheduled early.  Both are no-ops
+// when the kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
 // ------------------------------------------------------------------- K1
 // grid = (column tiles, row blocks); thread owns columns [c0, c0+VEC) over
@@ -78,6 +144,8 @@ __device__ __forceinline__ void store_stream(T* p, const T (&o)[VEC]) {
 template <typename T, int VEC, int Q, int U>
 __global__ void __launch_bounds__(kThreads)
     k_colnorm(const T* __restrict__ y, int64_t n, int64_t m, int64_t rpb, void* __restrict__ out) {
+  pdl_trigger();  // let the (single-CTA) outer kernel be scheduled as SMs free up
+  tl_begin(0);
   const int64_t c0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * VEC;
   if (c0 >= m) return;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rpb;
@@ -107,6 +175,7 @@ __global__ void __launch_bounds__(kThreads)
     B* vb = static_cast<B*>(out) + c0;
 #pragma unroll
     for (int j = 0; j < VEC; ++j) atomicMax(vb + j, acc[j]);
+    tl_end(0);
   } else {
     double acc[VEC];
 #pragma unroll
@@ -135,6 +204,7 @@ __global__ void __launch_bounds__(kThreads)
     double* part = static_cast<double*>(out) + static_cast<int64_t>(blockIdx.y) * m + c0;
 #pragma unroll
     for (int j = 0; j < VEC; ++j) part[j] = acc[j];
+    tl_end(0);
   }
 }
 
@@ -143,6 +213,9 @@ __global__ void __launch_bounds__(kThreads)
 template <int Q>
 __global__ void k_colnorm_finalize(const void* __restrict__ in, int64_t R, int64_t m, int bits_kind,
                                    double* __restrict__ v) {
+  pdl_wait();
+  pdl_trigger();
+  tl_begin(1);
   const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= m) return;
   if constexpr (Q == kInf) {
@@ -156,6 +229,39 @@ __global__ void k_colnorm_finalize(const void* __restrict__ in, int64_t R, int64
     for (int64_t r = 0; r < R; ++r) s = __dadd_rn(s, part[r * m + c]);
     v[c] = (Q == kL2) ? sqrt(s) : s;
   }
+  tl_end(1);
+}
+
+// l1 / l2 partials -> norms with 8 warps per 32 columns: warp w sums rows
+// w, w+8, ... (coalesced 32-column rows), then warp 0 adds the 8 warp sums in
+// fixed order (deterministic).
+template <int Q>
+__global__ void __launch_bounds__(256) k_colnorm_reduce(const double* __restrict__ part, int64_t R, int64_t m,
+                                                        double* __restrict__ v) {
+  pdl_wait();
+  pdl_trigger();
+  tl_begin(1);
+  __shared__ double red[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+  double s0 = 0.0, s1 = 0.0;
+  if (c < m) {
+    int64_t r = w;
+    for (; r + 8 < R; r += 16) {
+      s0 = __dadd_rn(s0, part[r * m + c]);
+      s1 = __dadd_rn(s1, part[(r + 8) * m + c]);
+    }
+    if (r < R) s0 = __dadd_rn(s0, part[r * m + c]);
+  }
+  red[w][lane] = __dadd_rn(s0, s1);
+  __syncthreads();
+  if (w == 0 && c < m) {
+    double s = red[0][lane];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) s = __dadd_rn(s, red[k][lane]);
+    v[c] = (Q == kL2) ? sqrt(s) : s;
+  }
+  tl_end(1);
 }
 
 // ------------------------------------------------------- reductions (K2)
@@ -246,6 +352,27 @@ __device__ __forceinline__ int block_or(int v, int* scr) {
 
 // ------------------------------------------------------------------- K2
 // Outer projection of a length-m vector held in shared memory.
+// Outcome of the outer projection, enough to derive every budget from its
+// norm: u = derive_u(P, v).  Written by K2, read by the apply kernels.
+struct OuterParams {
+  int mode;      // 0 identity, 1 zero, 2 l1 threshold tau, 3 l2 scale, 4 linf clip at eta
+  int pad;
+  double tau, scale, eta;
+};
+
+__device__ __forceinline__ double derive_u(const OuterParams& P, double x) {
+  switch (P.mode) {
+    case 1: return 0.0;
+    case 2: {
+      const double d = fabs(x) - P.tau;  // proj/src/vector_balls.cpp:42-48
+      return d > 0.0 ? copysign(d, x) : 0.0;
+    }
+    case 3: return x * P.scale;                                 // :171-177
+    case 4: return fabs(x) > P.eta ? copysign(P.eta, x) : x;  // :187-191
+    default: return x;
+  }
+}
+
 struct OuterArgs {
   const void* vin;   // input vector
   int vkind;         // 0: float |y| bits (K1 l_inf over f32), 1: double, 2: float values
@@ -258,10 +385,21 @@ struct OuterArgs {
   double* factor;    // nullable: per column u/v (v > u) or 1 for the l2 apply
   mp_info* info;     // required
   void* scratch;     // k_outer_large only: LargeScratch in the workspace
+  OuterParams* params;  // nullable: mode / tau / scale for derive_u
+  int emit;          // 1: write the per-element outputs above; 0: params + info only
 };
 
+__device__ __forceinline__ void outer_publish(const OuterArgs& a, int mode, double tau, double scale) {
+  if (a.params) {
+    a.params->mode = mode;
+    a.params->tau = tau;
+    a.params->scale = scale;
+    a.params->eta = a.eta;
+  }
+}
+
 constexpr int kOuterMaxPerThread = 24;
-constexpr int64_t kOuterMaxM = static_cast<int64_t>(kOuterThreads) * kOuterMaxPerThread;
+constexpr int64_t kOuterMaxM = static_cast<int64_t>(kOuterThreads) * kOuterMaxPerThread * kOuterMaxCluster;
 
 __device__ __forceinline__ double outer_load(const OuterArgs& a, int64_t i) {
   if (a.vkind == 0) return static_cast<double>(__uint_as_float(static_cast<const unsigned int*>(a.vin)[i]));
@@ -269,26 +407,281 @@ __device__ __forceinline__ double outer_load(const OuterArgs& a, int64_t i) {
   return static_cast<double>(static_cast<const float*>(a.vin)[i]);
 }
 
+__device__ __forceinline__ void block_sum_icount(double& s, int& c, double* sscr, int* cscr) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  __syncthreads();
+  if (lane == 0) {
+    sscr[w] = s;
+    cscr[w] = c;
+  }
+  __syncthreads();
+  s = (lane < (blockDim.x >> 5)) ? sscr[lane] : 0.0;
+  c = (lane < (blockDim.x >> 5)) ? cscr[lane] : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+}
+
+// Cluster-wide (sum, count): CTA reduction, then every thread reads the C
+// per-CTA partials through DSMEM in rank order (identical, deterministic
+// totals in every CTA).  Double-buffered partials: one cluster barrier per
+// reduction.
+__device__ __forceinline__ void cluster_sum_icount(double& s, int& c, double* sscr, int* cscr, double* ps,
+                                                   int* pc, int& par, const cg::cluster_group& cl, int C) {
+  block_sum_icount(s, c, sscr, cscr);
+  if (threadIdx.x == 0) {
+    ps[par] = s;
+    pc[par] = c;
+  }
+  cl.sync();
+  // lane r fetches CTA r's partial (all DSMEM loads in flight at once), then
+  // the same xor butterfly in every warp of every CTA => identical totals.
+  const int lane = threadIdx.x & 31;
+  double S = lane < C ? *cl.map_shared_rank(&ps[par], lane) : 0.0;
+  int N = lane < C ? *cl.map_shared_rank(&pc[par], lane) : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    S += __shfl_xor_sync(0xffffffffu, S, o);
+    N += __shfl_xor_sync(0xffffffffu, N, o);
+  }
+  par ^= 1;
+  s = S;
+  c = N;
+}
+
+// K2: the outer projection of the length-m norm vector
+// (proj/src/vector_balls.cpp:150-191,207-214) on a thread-block CLUSTER of C
+// CTAs (C <= 16): CTA r holds the r-th contiguous chunk of v in its shared
+// memory, P elements per thread (compile time: every per-element loop is
+// unrolled with constant shifts on the active-set mask).  A single CTA spent
+// ~14 us here on one SM's issue slots; spreading the vector over C SMs keeps
+// every pass to a few instructions per thread plus one DSMEM reduction.
+// Michelot (tau_{t+1} = (sum_{A_t} |v| - eta) / |A_t|, A_{t+1} = A_t cap
+// {|v| > tau_{t+1}}) converges when the active set stops shrinking; the
+// converged A equals the reference's {|v| >= cutoff} (cutoff = min A), so
+// the last pass's (sum, count) give tau directly.
+template <int P>
 __global__ void __launch_bounds__(kOuterThreads) k_outer(OuterArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  tl_begin(2);
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = static_cast<int>(cl.num_blocks());
+  const int rank = static_cast<int>(cl.block_rank());
   extern __shared__ double sv[];
-  __shared__ DD dscr[32];
   __shared__ double sscr[32];
-  __shared__ long long cscr[32];
+  __shared__ int cscr[32];
+  __shared__ double cps[2];
+  __shared__ int cpc[2];
+  int par = 0;
   const int tid = threadIdx.x;
-  const int64_t m = a.m;
+  const int m = static_cast<int>(a.m);
+  const int chunk = (m + C - 1) / C;
+  const int base = rank * chunk;
+  const int cnt = max(0, min(chunk, m - base));
   const double eta = a.eta;
 
-  // Load + finiteness + the feasibility / norm sum (double-double).
+  double s = 0.0;
   int bad = 0;
-  DD acc{0.0, 0.0};
-  for (int64_t i = tid; i < m; i += kOuterThreads) {
-    const double x = outer_load(a, i);
-    sv[i] = x;
-    bad |= !isfinite(x);
-    if (a.p == kL2) acc = dd_add(acc, dd_sq(x));
-    else acc = dd_add(acc, fabs(x));
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    const int i = tid + j * kOuterThreads;
+    if (i < cnt) {
+      const double x = outer_load(a, base + i);
+      sv[i] = x;
+      bad += !isfinite(x);
+      s += (a.p == kL2) ? x * x : fabs(x);
+    }
   }
-  bad = __syncthreads_or(bad);
+  cluster_sum_icount(s, bad, sscr, cscr, cps, cpc, par, cl, C);
+  if (bad) {
+    if (rank == 0 && tid == 0) {
+      a.info->status = MP_ERR_VALUE;
+      a.info->tau = -1.0;
+      a.info->active = -1;
+      a.info->iterations = 0;
+    }
+    cl.sync();
+    return;
+  }
+
+  // mode: 0 identity, 1 zero, 2 l1 threshold tau, 3 l2 scale, 4 linf clip
+  int mode = 0;
+  double tau = -1.0, scale = 1.0;
+  int active = -1;
+  int iters = 0;
+  if (a.p == kInf) {
+    mode = 4;
+  } else if (a.p == kL2) {
+    const double norm = sqrt(s);
+    if (!(norm <= eta) && norm != 0.0) {
+      mode = 3;
+      scale = eta / norm;
+    }
+  } else if (m > 0 && !(s <= eta)) {
+    if (eta == 0.0) {
+      mode = 1;
+      tau = 0.0;
+      active = 0;
+    } else {
+      mode = 2;
+      unsigned long long mask = 0;
+#pragma unroll
+      for (int j = 0; j < P; ++j)
+        if (tid + j * kOuterThreads < cnt) mask |= 1ull << j;
+      double t = (s - eta) / static_cast<double>(m);
+      int kprev = m;
+      double S = s;
+      for (;;) {
+        double ps = 0.0;
+        int pc = 0;
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+          if (mask >> j & 1ull) {
+            const double x = fabs(sv[tid + j * kOuterThreads]);
+            const bool keep = x > t;
+            ps += keep ? x : 0.0;
+            pc += keep;
+            if (!keep) mask &= ~(1ull << j);
+          }
+        }
+        cluster_sum_icount(ps, pc, sscr, cscr, cps, cpc, par, cl, C);
+        ++iters;
+        if (pc == 0) break;  // cannot happen for eta > 0; keep the last set
+        S = ps;
+        const bool stable = (pc == kprev);
+        kprev = pc;
+        if (stable) break;
+        t = (ps - eta) / static_cast<double>(pc);
+      }
+      active = kprev;
+      tau = (S - eta) / static_cast<double>(active);
+    }
+  }
+
+  if (rank == 0 && tid == 0) outer_publish(a, mode, tau, scale);
+  double zs = 0.0;  // zero-column count (exact in f64)
+  int surv = 0;
+  if (a.emit) {
+  double* __restrict__ uo = a.u_out + base;
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    const int i = tid + j * kOuterThreads;
+    if (i < cnt) {
+      const double x = sv[i];
+      double u = x;
+      if (mode == 2) {
+        const double dd = fabs(x) - tau;
+        u = dd > 0.0 ? copysign(dd, x) : 0.0;
+      } else if (mode == 4) {
+        u = fabs(x) > eta ? copysign(eta, x) : x;
+      } else if (mode == 3) {
+        u = x * scale;
+      } else if (mode == 1) {
+        u = 0.0;
+      }
+      uo[i] = u;
+      zs += (u == 0.0 || x == 0.0) ? 1.0 : 0.0;
+      surv += (u != 0.0);
+      sv[i] = u;  // keep u for the optional side outputs below
+    }
+  }
+  if (a.v_out || a.rdrn || a.factor) {
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const int i = tid + j * kOuterThreads;
+      if (i < cnt) {
+        const double u = sv[i];
+        if (a.rdrn) a.rdrn[base + i] = make_float2(__double2float_rz(u), __double2float_rn(u));
+        if (a.v_out || a.factor) {
+          const double x = outer_load(a, base + i);
+          if (a.v_out) a.v_out[base + i] = x;
+          if (a.factor) a.factor[base + i] = (x > u) ? u / x : 1.0;
+        }
+      }
+    }
+  }
+  }
+  cluster_sum_icount(zs, surv, sscr, cscr, cps, cpc, par, cl, C);
+  if (rank == 0 && tid == 0) {
+    a.info->status = MP_OK;
+    a.info->tau = tau;
+    a.info->active = active;
+    a.info->iterations = iters;
+    a.info->zero_columns = static_cast<long long>(zs);
+    a.info->survivors = surv;
+  }
+  cl.sync();  // no CTA leaves while a peer may still read its DSMEM
+  tl_end(2);
+}
+
+// Block all-reduce of (sum, count) with ONE barrier: double-buffered warp
+// slots; every warp re-reduces the 32 slots with the same xor butterfly, so
+// every thread ends with the same bits (a + b == b + a exactly).
+__device__ __forceinline__ void block_allreduce(double& s, int& c, double (*sb)[32], int (*cb)[32], int& par) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  if (lane == 0) {
+    sb[par][w] = s;
+    cb[par][w] = c;
+  }
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  s = lane < nw ? sb[par][lane] : 0.0;
+  c = lane < nw ? cb[par][lane] : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  par ^= 1;
+}
+
+constexpr int kOuterRegThreads = 1024;
+constexpr int kOuterRegMaxP = 12;
+constexpr int64_t kOuterRegMaxM = static_cast<int64_t>(kOuterRegThreads) * kOuterRegMaxP;
+
+// K2 fast path (m <= 16384): ONE CTA of 1024 threads, the vector held in
+// registers (P per thread, compile time), every reduction a single-barrier
+// all-reduce.  The kernel's time is its dependency chain on one SM: a load
+// wave, 1 + passes + 1 block reductions, one double division per pass.
+template <int P>
+__global__ void __launch_bounds__(kOuterRegThreads, 1) k_outer_reg(OuterArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  tl_begin(2);
+  __shared__ double sb[2][32];
+  __shared__ int cb[2][32];
+  int par = 0;
+  const int tid = threadIdx.x;
+  const int m = static_cast<int>(a.m);
+  const double eta = a.eta;
+
+  double v[P];
+  double s = 0.0;
+  int bad = 0;
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    const int i = tid + j * kOuterRegThreads;
+    v[j] = (i < m) ? outer_load(a, i) : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    bad += !isfinite(v[j]);
+    s += (a.p == kL2) ? v[j] * v[j] : fabs(v[j]);
+  }
+  block_allreduce(s, bad, sb, cb, par);
   if (bad) {
     if (tid == 0) {
       a.info->status = MP_ERR_VALUE;
@@ -298,148 +691,193 @@ __global__ void __launch_bounds__(kOuterThreads) k_outer(OuterArgs a) {
     }
     return;
   }
-  const DD total = block_sum_dd(acc, dscr);
 
-  // mode: 0 identity, 1 zero, 2 l1 threshold tau, 3 l2 scale, 4 linf clip
-  int mode = 0;
+  int mode = 0;  // 0 identity, 1 zero, 2 l1 threshold, 3 l2 scale, 4 linf clip
   double tau = -1.0, scale = 1.0;
-  long long active = -1;
-  int iters = 0;
+  int active = -1, iters = 0;
   if (a.p == kInf) {
     mode = 4;
   } else if (a.p == kL2) {
-    const double norm = sqrt(dd_value(total));
+    const double norm = sqrt(s);
     if (!(norm <= eta) && norm != 0.0) {
       mode = 3;
       scale = eta / norm;
     }
-  } else if (m > 0 && !(dd_value(total) <= eta)) {
+  } else if (m > 0 && !(s <= eta)) {
     if (eta == 0.0) {
       mode = 1;
       tau = 0.0;
       active = 0;
     } else {
       mode = 2;
-      // Michelot fixed point on a monotonically shrinking active set.
-      unsigned int mask = 0;
-      for (int j = 0; j < kOuterMaxPerThread; ++j)
-        if (tid + static_cast<int64_t>(j) * kOuterThreads < m) mask |= 1u << j;
-      double t = (dd_value(total) - eta) / static_cast<double>(m);
-      long long kprev = m;
+      unsigned mask = 0;
+#pragma unroll
+      for (int j = 0; j < P; ++j)
+        if (tid + j * kOuterRegThreads < m) mask |= 1u << j;
+      double t = (s - eta) / static_cast<double>(m);
+      int kprev = m;
+      double S = s;
       for (;;) {
-        double s = 0.0;
-        long long c = 0;
-#pragma unroll 4
-        for (int j = 0; j < kOuterMaxPerThread; ++j) {
-          if (!(mask >> j & 1u)) continue;
-          const double x = fabs(sv[tid + static_cast<int64_t>(j) * kOuterThreads]);
-          if (x > t) {
-            s = __dadd_rn(s, x);
-            ++c;
-          } else {
-            mask &= ~(1u << j);
-          }
+        double ps = 0.0;
+        int pc = 0;
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+          const double x = fabs(v[j]);
+          const bool keep = (mask >> j & 1u) && x > t;
+          ps += keep ? x : 0.0;
+          pc += keep;
+          mask = keep ? mask : (mask & ~(1u << j));
         }
-        block_sum_count(s, c, sscr, cscr);
+        block_allreduce(ps, pc, sb, cb, par);
         ++iters;
-        if (c == kprev || c == 0) break;
-        t = (s - eta) / static_cast<double>(c);
-        kprev = c;
+        if (pc == 0) break;  // cannot happen for eta > 0; keep the last set
+        S = ps;
+        const bool stable = (pc == kprev);
+        kprev = pc;
+        if (stable) break;
+        t = (ps - eta) / static_cast<double>(pc);
       }
-      // Final threshold, reference definition: cutoff = smallest active
-      // magnitude, k = #{|v| >= cutoff}, tau = (sum_{|v|>=cutoff} |v| - eta)/k.
-      double lmin = __longlong_as_double(0x7ff0000000000000ll);
-      for (int j = 0; j < kOuterMaxPerThread; ++j)
-        if (mask >> j & 1u) lmin = fmin(lmin, fabs(sv[tid + static_cast<int64_t>(j) * kOuterThreads]));
-      const double cutoff = block_min(lmin, sscr);
-      DD ps{0.0, 0.0};
-      long long pk = 0;
-      for (int64_t i = tid; i < m; i += kOuterThreads) {
-        const double x = fabs(sv[i]);
-        if (x >= cutoff) {
-          ps = dd_add(ps, x);
-          ++pk;
-        }
-      }
-      const DD S = block_sum_dd(ps, dscr);
-      active = block_count(pk, cscr);
-      const DD d = two_sum(S.hi, -eta);
-      tau = __dadd_rn(d.hi, __dadd_rn(d.lo, S.lo)) / static_cast<double>(active);
+      active = kprev;
+      tau = (S - eta) / static_cast<double>(active);
     }
   }
 
-  long long zeros = 0, surv = 0;
-  for (int64_t i = tid; i < m; i += kOuterThreads) {
-    const double x = sv[i];
-    double u;
-    switch (mode) {
-      case 1: u = 0.0; break;
-      case 2: {
-        const double d = fabs(x) - tau;
-        u = d > 0.0 ? copysign(d, x) : 0.0;
-        break;
+  if (tid == 0) outer_publish(a, mode, tau, scale);
+  double zs = 0.0;
+  int surv = 0;
+  if (a.emit) {
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const int i = tid + j * kOuterRegThreads;
+      if (i < m) {
+        const double x = v[j];
+        double u = x;
+        if (mode == 2) {
+          const double dd = fabs(x) - tau;
+          u = dd > 0.0 ? copysign(dd, x) : 0.0;
+        } else if (mode == 4) {
+          u = fabs(x) > eta ? copysign(eta, x) : x;
+        } else if (mode == 3) {
+          u = x * scale;
+        } else if (mode == 1) {
+          u = 0.0;
+        }
+        a.u_out[i] = u;
+        if (a.v_out) a.v_out[i] = x;
+        if (a.rdrn) a.rdrn[i] = make_float2(__double2float_rz(u), __double2float_rn(u));
+        if (a.factor) a.factor[i] = (x > u) ? u / x : 1.0;
+        zs += (u == 0.0 || x == 0.0) ? 1.0 : 0.0;
+        surv += (u != 0.0);
       }
-      case 3: u = x * scale; break;
-      case 4: u = fabs(x) > eta ? copysign(eta, x) : x; break;
-      default: u = x;
     }
-    a.u_out[i] = u;
-    if (a.v_out) a.v_out[i] = x;
-    zeros += (u == 0.0 || x == 0.0);
-    surv += (u != 0.0);
-    if (a.rdrn) a.rdrn[i] = make_float2(__double2float_rz(u), __double2float_rn(u));
-    if (a.factor) a.factor[i] = (x > u) ? u / x : 1.0;
+    block_allreduce(zs, surv, sb, cb, par);
   }
-  zeros = block_count(zeros, cscr);
-  surv = block_count(surv, cscr);
   if (tid == 0) {
     a.info->status = MP_OK;
     a.info->tau = tau;
     a.info->active = active;
     a.info->iterations = iters;
-    a.info->zero_columns = zeros;
+    a.info->zero_columns = static_cast<long long>(zs);  // emit = 0: the apply pass accumulates them
     a.info->survivors = surv;
   }
+  tl_end(2);
 }
 
 // ------------------------------------------------------------------- K3
+// Per-column inputs of the apply pass.  DERIVE (the bi-level hot path): each
+// thread derives its columns' budgets from the norms and K2's OuterParams --
+// u = derive_u(P, v) -- so K2 stays a short serial step and the per-column
+// work is spread over the whole grid; row block 0 also writes the user-facing
+// budgets / norms and accumulates zero_columns / survivors.  Otherwise
+// (multi-level levels): precomputed colp (float2 {RD(u), RN(u)} for f32
+// l_inf, double u for f64 l_inf, double factor for l2) and budgets.
+struct ApplyCols {
+  const void* colp;
+  const double* budgets;
+  const void* v;          // DERIVE: norms (vkind 0: float |y| bits, 1: double)
+  int vkind;
+  const OuterParams* params;
+  double* u_out;          // DERIVE, nullable
+  double* v_out;          // DERIVE, nullable
+  mp_info* info_w;        // DERIVE: zero_columns / survivors accumulators
+};
+
+__device__ __forceinline__ double load_norm(const ApplyCols& a, int64_t c) {
+  return a.vkind == 0 ? static_cast<double>(__uint_as_float(static_cast<const unsigned int*>(a.v)[c]))
+                      : static_cast<const double*>(a.v)[c];
+}
+
 // l_inf clamp (proj/src/fiber_kernels.cpp:43-49) / l2 scale (:50-55).
-// colp: float2 {RD(u), RN(u)} (f32 l_inf), double u (f64 l_inf) or double
-// factor (l2).  `dead` columns (u == 0) are written as +0 without a read
-// unless MP_FLAG_EXACT_ZERO_SIGN.
-template <typename T, int VEC, int Q, int U>
+// `dead` column groups (u == 0) are written as +0 without a read unless
+// MP_FLAG_EXACT_ZERO_SIGN.
+template <typename T, int VEC, int Q, int U, bool DERIVE>
 __global__ void __launch_bounds__(kThreads)
-    k_apply(const T* __restrict__ y, T* __restrict__ x, int64_t n, int64_t m, int64_t rpb, int nrb,
-            const void* __restrict__ colp, const double* __restrict__ budgets,
+    k_apply(const T* __restrict__ y, T* __restrict__ x, int64_t n, int64_t m, int64_t rpb, ApplyCols A,
             const mp_info* __restrict__ info, unsigned flags) {
+  pdl_wait();
+  tl_begin(3);
   if (info->status != MP_OK) return;
   const int64_t c0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * VEC;
   if (c0 >= m) return;
-  const int64_t rb = static_cast<int64_t>(nrb) - 1 - blockIdx.y;  // reverse sweep: L2 tail reuse
-  const int64_t r0 = rb * rpb;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rpb;
   const int64_t r1 = min(n, r0 + rpb);
 
   // per-column parameters
   float rd[VEC], rn[VEC];
   double pu[VEC];
   bool dead = !(flags & MP_FLAG_EXACT_ZERO_SIGN);
+  if constexpr (DERIVE) {
+    const OuterParams P = *A.params;
+    unsigned long long zc = 0, sv = 0;
 #pragma unroll
-  for (int j = 0; j < VEC; ++j) {
-    if constexpr (Q == kInf && sizeof(T) == 4) {
-      const float2 q = static_cast<const float2*>(colp)[c0 + j];
-      rd[j] = q.x;
-      rn[j] = q.y;
-    } else {
-      pu[j] = static_cast<const double*>(colp)[c0 + j];
+    for (int j = 0; j < VEC; ++j) {
+      const double vj = load_norm(A, c0 + j);
+      const double uj = derive_u(P, vj);
+      if constexpr (Q == kInf && sizeof(T) == 4) {
+        rd[j] = __double2float_rz(uj);
+        rn[j] = __double2float_rn(uj);
+      } else if constexpr (Q == kInf) {
+        pu[j] = uj;
+      } else {
+        pu[j] = (vj > uj) ? uj / vj : 1.0;
+      }
+      dead = dead && (uj == 0.0);
+      if (blockIdx.y == 0) {
+        if (A.u_out) A.u_out[c0 + j] = uj;
+        if (A.v_out) A.v_out[c0 + j] = vj;
+        zc += (uj == 0.0 || vj == 0.0);
+        sv += (uj != 0.0);
+      }
     }
-    dead = dead && (budgets[c0 + j] == 0.0);
+    if (blockIdx.y == 0) {
+      if (zc) atomicAdd(reinterpret_cast<unsigned long long*>(&A.info_w->zero_columns), zc);
+      if (sv) atomicAdd(reinterpret_cast<unsigned long long*>(&A.info_w->survivors), sv);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      if constexpr (Q == kInf && sizeof(T) == 4) {
+        const float2 q = static_cast<const float2*>(A.colp)[c0 + j];
+        rd[j] = q.x;
+        rn[j] = q.y;
+      } else {
+        pu[j] = static_cast<const double*>(A.colp)[c0 + j];
+      }
+      dead = dead && (A.budgets[c0 + j] == 0.0);
+    }
   }
-  T* q = x + r0 * m + c0;
+  if (r1 <= r0) return;
+  // Rows are swept from the END of the block backwards: K1 swept the same
+  // blocks forwards in one resident wave, so the last rows of each block are
+  // the ones still in L2 when this kernel starts.
+  const int64_t last = (r1 - 1) * m + c0;
+  T* q = x + last;
   if (dead) {
     T z[VEC];
 #pragma unroll
     for (int j = 0; j < VEC; ++j) z[j] = T(0);
-    for (int64_t r = r0; r < r1; ++r, q += m) store_stream<T, VEC>(q, z);
+    for (int64_t r = r1; r > r0; --r, q -= m) store_stream<T, VEC>(q, z);
+    tl_end(3);
     return;
   }
   auto op = [&](T e, int j) -> T {
@@ -451,26 +889,27 @@ __global__ void __launch_bounds__(kThreads)
       else return __dmul_rn(e, pu[j]);
     }
   };
-  const T* p = y + r0 * m + c0;
-  int64_t r = r0;
-  for (; r + U <= r1; r += U, p += U * m, q += U * m) {
+  const T* p = y + last;
+  int64_t r = r1;
+  for (; r - U >= r0; r -= U, p -= U * m, q -= U * m) {
     T e[U][VEC];
 #pragma unroll
-    for (int u = 0; u < U; ++u) load_last<T, VEC>(p + u * m, e[u]);
+    for (int u = 0; u < U; ++u) load_last<T, VEC>(p - u * m, e[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
 #pragma unroll
       for (int j = 0; j < VEC; ++j) e[u][j] = op(e[u][j], j);
-      store_stream<T, VEC>(q + u * m, e[u]);
+      store_stream<T, VEC>(q - u * m, e[u]);
     }
   }
-  for (; r < r1; ++r, p += m, q += m) {
+  for (; r > r0; --r, p -= m, q -= m) {
     T e[VEC];
     load_last<T, VEC>(p, e);
 #pragma unroll
     for (int j = 0; j < VEC; ++j) e[j] = op(e[j], j);
     store_stream<T, VEC>(q, e);
   }
+  tl_end(3);
 }
 
 }  // namespace mpk

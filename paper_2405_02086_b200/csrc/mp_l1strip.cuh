@@ -27,6 +27,7 @@
 #include "mp_cuda.h"
 #include "mp_internal.h"
 #include "mp_kernels.cuh"
+#include "mp_l1cols.cuh"
 
 namespace mpk {
 
@@ -93,6 +94,7 @@ __global__ void __launch_bounds__(kStripThreads)
     k_l1strip(const T* __restrict__ y, T* __restrict__ x, int64_t n, int64_t m, int64_t rpc,
               const double* __restrict__ v, const double* __restrict__ u, double* __restrict__ tau_out,
               const mp_info* __restrict__ info, unsigned flags) {
+  tl_begin(3);
   if (info->status != MP_OK) return;  // uniform across the cluster
   cg::cluster_group cl = cg::this_cluster();
   const unsigned C = cl.num_blocks();
@@ -120,6 +122,7 @@ __global__ void __launch_bounds__(kStripThreads)
       else if (kind == 2) x[idx] = T(0);
     }
     if (rank == 0 && warp == 0 && colok) tau_out[col] = -1.0;
+    tl_end(3);
     return;
   }
 
@@ -241,56 +244,86 @@ __global__ void __launch_bounds__(kStripThreads)
       x[idx] = d > 0.0 ? static_cast<T>(copysign(d, static_cast<double>(e))) : T(0);
     }
   }
+  tl_end(3);
 }
 
-struct StripPlan {
-  bool staged;
-  unsigned C;
-  int64_t rpc;
-  size_t smem;
+constexpr size_t kColsSmemTarget = 72 * 1024;   // >= 3 CTAs per SM
+constexpr size_t kColsSmemMax = 200 * 1024;
+
+template <typename T>
+inline int cols_stride(int64_t n) {
+  return static_cast<int>(((n + 3) / 4) * 4 + 4);  // 16-byte aligned columns, offset banks
+}
+
+template <typename T, int W>
+cudaError_t cols_attr() {
+  cudaError_t e = cudaFuncSetAttribute(k_l1cols<T, W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kColsSmemMax));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_l1cols<T, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(kColsSmemMax));
+}
+
+// K2 outcome handed to the l1 apply when it derives the budgets itself.
+struct L1Derive {
+  const OuterParams* params = nullptr;  // null: read budgets u[]
+  double* u_out = nullptr;
+  mp_info* info_w = nullptr;
 };
 
-inline StripPlan plan_l1strip(int64_t n, size_t elem) {
-  const size_t rowb = kStripCols * elem;
-  for (unsigned C : {1u, 2u, 4u, 8u, 16u}) {
-    const int64_t rpc = (n + C - 1) / C;
-    if (static_cast<size_t>(rpc) * rowb <= kStripTileMax) return {true, C, rpc, static_cast<size_t>(rpc) * rowb};
-  }
-  return {false, 1u, n, 0};
-}
-
 inline cudaError_t l1strip_setup() {
-  cudaError_t e;
-  for (auto fn : {reinterpret_cast<const void*>(k_l1strip<float, true>),
-                  reinterpret_cast<const void*>(k_l1strip<double, true>)}) {
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kStripTileMax));
+  for (cudaError_t e : {cols_attr<float, 8>(), cols_attr<float, 4>(), cols_attr<float, 2>(), cols_attr<float, 1>(),
+                        cols_attr<double, 8>(), cols_attr<double, 4>(), cols_attr<double, 2>(),
+                        cols_attr<double, 1>()})
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-  }
   return cudaSuccess;
 }
 
+template <typename T, int W>
+cudaError_t launch_cols(const T* y, T* x, int64_t n, int64_t m, const double* v, const double* u,
+                        const L1StripWs& ws, const mp_info* info, const L1Derive& dv, cudaStream_t s) {
+  const int stride = cols_stride<T>(n);
+  const size_t smem = static_cast<size_t>(W) * stride * sizeof(T);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>((m + W - 1) / W));
+  cfg.blockDim = dim3(32 * W);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (dv.params)
+    return cudaLaunchKernelEx(&cfg, k_l1cols<T, W, true>, y, x, static_cast<int>(n), m, stride, v, u, ws.tau, info,
+                              dv.params, dv.u_out, dv.info_w);
+  return cudaLaunchKernelEx(&cfg, k_l1cols<T, W, false>, y, x, static_cast<int>(n), m, stride, v, u, ws.tau, info,
+                            dv.params, dv.u_out, dv.info_w);
+}
+
+// Per-column l1 projection: warp-per-column staged kernel when a column
+// fits shared memory (n up to ~50k f32 rows), else the unstaged strip
+// kernel (passes re-read the strip from L2).
+template <typename T>
+inline bool l1_staged_ok(int64_t n) {
+  return static_cast<size_t>(cols_stride<T>(n)) * sizeof(T) <= kColsSmemMax;
+}
+
+// With dv.params set, u must still point at a budgets array the fallback
+// path can read; the staged kernels derive the budgets themselves.
 template <typename T>
 cudaError_t launch_l1strip(const T* y, T* x, int64_t n, int64_t m, const double* v, const double* u,
-                           const L1StripWs& ws, const mp_info* info, unsigned flags, cudaStream_t s) {
-  const StripPlan pl = plan_l1strip(n, sizeof(T));
+                           const L1StripWs& ws, const mp_info* info, unsigned flags, cudaStream_t s,
+                           const L1Derive& dv = L1Derive()) {
+  const size_t col_bytes = static_cast<size_t>(cols_stride<T>(n)) * sizeof(T);
+  if (8 * col_bytes <= kColsSmemTarget) return launch_cols<T, 8>(y, x, n, m, v, u, ws, info, dv, s);
+  if (4 * col_bytes <= kColsSmemTarget) return launch_cols<T, 4>(y, x, n, m, v, u, ws, info, dv, s);
+  if (2 * col_bytes <= kColsSmemTarget) return launch_cols<T, 2>(y, x, n, m, v, u, ws, info, dv, s);
+  if (col_bytes <= kColsSmemMax) return launch_cols<T, 1>(y, x, n, m, v, u, ws, info, dv, s);
   const int64_t nstrips = (m + kStripCols - 1) / kStripCols;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(nstrips * pl.C));
-  cfg.blockDim = dim3(kStripThreads);
-  cfg.dynamicSmemBytes = pl.smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = pl.C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (pl.staged)
-    return cudaLaunchKernelEx(&cfg, k_l1strip<T, true>, y, x, n, m, pl.rpc, v, u, ws.tau, info, flags);
-  return cudaLaunchKernelEx(&cfg, k_l1strip<T, false>, y, x, n, m, pl.rpc, v, u, ws.tau, info, flags);
+  k_l1strip<T, false><<<static_cast<unsigned>(nstrips), kStripThreads, 0, s>>>(y, x, n, m, n, v, u, ws.tau, info,
+                                                                              flags);
+  return cudaGetLastError();
 }
 
 }  // namespace mpk

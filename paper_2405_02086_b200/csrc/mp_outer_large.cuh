@@ -166,8 +166,9 @@ __global__ void __launch_bounds__(kLargeThreads) k_outer_large(OuterArgs a, Larg
     }
   }
 
+  if (b == 0 && threadIdx.x == 0) outer_publish(a, mode, tau, scale);
   long long zeros = 0, surv = 0;
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+  for (int64_t i = i0 + threadIdx.x; i < i1 && a.emit; i += blockDim.x) {
     const double x = outer_load(a, i);
     double u;
     switch (mode) {

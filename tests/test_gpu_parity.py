@@ -201,13 +201,17 @@ def test_ragged_and_unaligned():
             check_bilevel(x, y, oracle_bilevel(y, eta, "1", q), q, zero_cols_gpu=z)
 
 
-def test_large_m_cooperative_outer():
-    """m > 24576: the outer l1 projection runs as a cooperative grid."""
-    y = datagen.normal(12, (3, 70000))
+@pytest.mark.parametrize("m", [2049, 9999, 70000, 130000])
+def test_wide_outer_cluster_and_cooperative(m):
+    """K2 on 1..16-CTA clusters (m <= 98304) and as a cooperative grid beyond."""
+    y = datagen.normal(12, (3, m))
     for q in NORMS:
         eta = 0.05 * O.matrix_pq_norm(y.astype(np.float64), "1", q)
         x, b, z = run(y, eta, "1", q)
         check_bilevel(x, y, oracle_bilevel(y, eta, "1", q), q, zero_cols_gpu=z)
+
+
+def test_large_vector_ball():
     v = datagen.normal(13, (300001,)).astype(np.float64)
     for q in NORMS:
         r = 0.1 * O.multilevel_norm(v, [q])
