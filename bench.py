@@ -215,19 +215,31 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.Stream(dev)
     nproj = len(etas)
     lib = _capi.lib()
-    # One CUDA graph per projection (memset + K1 + K2 + K3 replayed as a unit);
-    # timing events are recorded on the stream OUTSIDE the graphs, the L2
-    # flush runs between them.
-    graphs = []
+    # ONE CUDA graph per step: [L2 flush, projection] x 4.  The library
+    # records a timing event before each projection's first node and after its
+    # last (external event nodes), so the step's projections are timed on the
+    # device without the flushes and without per-replay launch overhead.  (No
+    # events between the kernels: an event node there would break the PDL
+    # edges K1 -> K2 -> K3.)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nproj)]
+
+    def one_step():
+        for k, e in enumerate(etas):
+            flush.zero_()
+            handles = (C.c_void_p * 4)(C.c_void_p(ev[k][0].cuda_event), None, None, C.c_void_p(ev[k][1].cuda_event))
+            lib.mp_profile_events(handles, 4)
+            proj(y, x, e, stream=stream)
+            lib.mp_profile_events(None, 0)
+
     with torch.cuda.stream(stream):
-        for e in etas:
-            proj(y, x, e, stream=stream)  # eager warm call
+        for row in ev:
+            for v in row:
+                v.record(stream)  # materialise the events before capture
+        one_step()  # eager warm call
         torch.cuda.synchronize()
-        for e in etas:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                proj(y, x, e, stream=stream)
-            graphs.append(g)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            one_step()
     torch.cuda.synchronize()
     # survivors per radius (device info after a plain run)
     f_surv, outer_iters = [], []
@@ -239,19 +251,9 @@ def run_ours(args, rank, world, local_rank):
         outer_iters.append(int(inf_.iterations))
     bytes_step = sum(algo_bytes(n, m, f) for f in f_surv)
     apply_bytes = [4.0 * n * m * (1.0 + f) for f in f_surv]  # K3: surviving reads + full write
-    ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(nproj)]
-    ev_b = [torch.cuda.Event(enable_timing=True) for _ in range(nproj)]
 
-    def timed_step():
-        for k in range(nproj):
-            flush.zero_()
-            ev_a[k].record(stream)
-            graphs[k].replay()
-            ev_b[k].record(stream)
-
-    with torch.cuda.stream(stream):
-        for _ in range(max(3, args.warmup)):
-            timed_step()
+    for _ in range(max(3, args.warmup)):
+        graph.replay()
     torch.cuda.synchronize()
     if dist:
         td.barrier()
@@ -265,9 +267,10 @@ def run_ours(args, rank, world, local_rank):
     with torch.cuda.stream(stream):
         wall0.record(stream)
         for _ in range(args.steps):
-            timed_step()
-            stream.synchronize()
-            t_proj += sum(ev_a[k].elapsed_time(ev_b[k]) for k in range(nproj))
+            graph.replay()
+            stream.synchronize()  # the step's events are re-recorded by every replay
+            for k in range(nproj):
+                t_proj += ev[k][0].elapsed_time(ev[k][1])
         wall1.record(stream)
     torch.cuda.synchronize()
     if dist:
@@ -281,42 +284,41 @@ def run_ours(args, rank, world, local_rank):
         ms_per_step = float(tt.item())
     value = world * bytes_step / (ms_per_step * 1e-3) / 1e9
 
-    # ---- per-phase device times (same kernels, eager, events recorded by
-    # the library at its phase boundaries through mp_profile_events)
-    ph = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nproj)]
-    t_k = [0.0, 0.0, 0.0]
-    phase_reps = max(3, min(args.steps, 20))
+    # ---- per-kernel device times from the kernels' own %globaltimer marks
+    # (mp_profile_timeline), one projection per radius, median of reps.
+    tl = torch.empty(8, dtype=torch.int64, device=dev)
+    kt = {"K1": [], "K2": [], "K3": [], "gaps": [], "span": []}
     with torch.cuda.stream(stream):
-        for row in ph:
-            for v in row:
-                v.record(stream)
-        for _ in range(phase_reps):
-            for k, e in enumerate(etas):
+        for rep in range(max(3, min(args.steps, 10))):
+            for e in etas:
+                tl.copy_(torch.tensor([2**63 - 1, 0] * 4, dtype=torch.int64))
+                lib.mp_profile_timeline(tl.data_ptr())
                 flush.zero_()
-                handles = (C.c_void_p * 4)(*[C.c_void_p(v.cuda_event) for v in ph[k]])
-                lib.mp_profile_events(handles, 4)
                 proj(y, x, e, stream=stream)
-                lib.mp_profile_events(None, 0)
-            stream.synchronize()
-            for k in range(nproj):
-                a, b, c, d_ = ph[k]
-                t_k[0] += a.elapsed_time(b)
-                t_k[1] += b.elapsed_time(c)
-                t_k[2] += c.elapsed_time(d_)
-    nphase = phase_reps * nproj
+                stream.synchronize()
+                lib.mp_profile_timeline(None)
+                t = tl.cpu().numpy().astype(np.float64) / 1e3  # us
+                kt["K1"].append(t[1] - t[0])
+                kt["K2"].append(t[5] - t[4])
+                kt["K3"].append(t[7] - t[6])
+                kt["gaps"].append((t[4] - t[1]) + (t[6] - t[5]))
+                kt["span"].append(t[7] - t[0])
+    med = {k: float(np.median(v)) for k, v in kt.items()}
 
     # ---- dominant kernel roofline: K3 (apply) per launch
     peak, peak_src = peaks()
-    del graphs
-    k3_ms = t_k[2] / nphase
+    del graph
+    k3_ms = med["K3"] * 1e-3
     k3_bytes = sum(apply_bytes) / nproj
     k3_gbs = k3_bytes / (k3_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": k3_gbs, "peak": peak, "unit": "GB/s", "frac": k3_gbs / peak,
                 "traffic": None, "kernel": "k_apply (K3, l_inf clamp)", "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": k3_bytes, "avg_launch_ms": k3_ms}
     call_gbs = bytes_step / (ms_per_step * 1e-3) / 1e9
-    phase_ms = {"norm_K1": t_k[0] / nphase, "outer_K2": t_k[1] / nphase, "apply_K3": k3_ms,
-                "note": "eager per-phase events (library-recorded), L2 flushed before each projection"}
+    phase_ms = {"norm_K1": med["K1"] * 1e-3, "outer_K2": med["K2"] * 1e-3, "apply_K3": k3_ms,
+                "inter_kernel_gaps": med["gaps"] * 1e-3, "K1_start_to_K3_end": med["span"] * 1e-3,
+                "note": "kernel spans from the kernels' own %globaltimer marks (first CTA start to last CTA "
+                        "end), eager single projections after an L2 flush; medians"}
     traffic_path = os.path.join(ROOT, "profiles", "k3_traffic.json")
     if os.path.exists(traffic_path):
         try:
@@ -376,11 +378,11 @@ def run_ours(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded xoshiro256++ U[-1,1], BASELINE config 2)",
             "config": {"workload": "config2: bilevel l1,inf 10000x10000 fp32, radius sweep {0.001,0.01,0.1,0.5}*||Y||",
-                       "step": "4 projections (one per radius), CUDA graph",
+                       "step": "4 projections (one per radius) in one CUDA graph, each preceded by an L2 flush",
                        "l2": "flushed before every projection by reading a 256 MiB buffer (2x L2); flush excluded by CUDA events; input 400 MB > L2",
                        "f_surv": f_surv, "outer_l1_passes": outer_iters, "bytes_per_step": bytes_step,
                        "pct_hbm_roofline_call": call_gbs / peak, "phase_ms": phase_ms,
-                       "wall_ms_incl_flush": wall_ms, "parallelism": f"replicas x{world}"},
+                       "wall_ms_incl_flush_and_event_reads": wall_ms, "parallelism": f"replicas x{world}"},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -21,7 +21,13 @@ static thread_local std::string g_err;
 static thread_local cudaEvent_t g_prof[4] = {nullptr, nullptr, nullptr, nullptr};
 
 void prof_mark(int i, cudaStream_t s) {
-  if (g_prof[i]) cudaEventRecord(g_prof[i], s);
+  if (!g_prof[i]) return;
+  // Inside stream capture, record an EXTERNAL event node so the event stays
+  // usable for timing after every graph replay.
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(g_prof[i], s, cudaEventRecordExternal);
+  else cudaEventRecord(g_prof[i], s);
 }
 
 void set_error(const char* fmt, ...) {
@@ -55,6 +61,8 @@ using namespace mpi;
 namespace {
 
 // ----------------------------------------------------------- grid planning
+constexpr int kRowInterleave = 1;  // see mpk::row_walk: the grid sweeps HBM band by band
+
 struct Grid {
   int vec = 1;
   int threads = 32;
@@ -125,14 +133,14 @@ int occupancy(const void* fn, int threads) {
 
 int pick_vec(mp_dtype dt, int64_t m, const void* a, const void* b) {
   const uintptr_t al = reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b);
-  // 32-byte packs (256-bit LDG/STG on sm_100) when rows stay 32-byte aligned
+  // 16-byte packs: measured on B200 (scripts/tune), 16-byte LDG at full
+  // occupancy streams faster than 256-bit LDG at the lower occupancy its
+  // register footprint allows (K1 64 us vs 74 us on 400 MB).
   if (dt == MP_F32) {
-    if (m % 8 == 0 && al % 32 == 0) return 8;
     if (m % 4 == 0 && al % 16 == 0) return 4;
     if (m % 2 == 0 && al % 8 == 0) return 2;
     return 1;
   }
-  if (m % 4 == 0 && al % 32 == 0) return 4;
   if (m % 2 == 0 && al % 16 == 0) return 2;
   return 1;
 }
@@ -150,26 +158,18 @@ int64_t max_nrb(mp_dtype dt, int64_t n, int64_t m) {
 }
 
 // --------------------------------------------------------------- dispatch
-// K1 and K3 of one projection share the row partition (the smaller of their
-// two occupancies), so every K3 CTA starts on exactly the rows its K1
-// counterpart read last -- still resident in L2.
-template <typename T, int VEC, int Q>
-int pair_occupancy(int threads) {
-  constexpr int QA = (Q == mpk::kL2) ? mpk::kL2 : mpk::kInf;
-  constexpr int U1 = (sizeof(T) * VEC == 32) ? 4 : 8;
-  const int o1 = occupancy(reinterpret_cast<const void*>(mpk::k_colnorm<T, VEC, Q, U1>), threads);
-  const int o3 = occupancy(reinterpret_cast<const void*>(mpk::k_apply<T, VEC, QA, 4, true>), threads);
-  return std::min(o1, o3);
-}
-
+// K1 and K3 each run one resident wave at their own occupancy.  Rows are
+// interleaved across the grid (kRowInterleave), so both kernels sweep HBM
+// band by band and K3's reverse sweep starts on the bands K1 read last --
+// still in L2 -- whatever the two grids are.
 template <typename T, int VEC, int Q>
 cudaError_t launch_colnorm_q(int64_t n, int64_t m, const T* y, void* out, Grid& g, cudaStream_t s) {
   constexpr int U = (sizeof(T) * VEC == 32) ? 4 : 8;  // 128 bytes of loads in flight per thread
   auto fn = mpk::k_colnorm<T, VEC, Q, U>;
   const int t = threads_for(VEC, m);
-  g = plan_grid(VEC, n, m, pair_occupancy<T, VEC, Q>(t));
+  g = plan_grid(VEC, n, m, occupancy(reinterpret_cast<const void*>(fn), t));
   dim3 grid(static_cast<unsigned>(g.ntiles), static_cast<unsigned>(g.nrb));
-  fn<<<grid, g.threads, 0, s>>>(y, n, m, g.rpb, out);
+  fn<<<grid, g.threads, 0, s>>>(y, n, m, kRowInterleave ? n / g.nrb : g.rpb, kRowInterleave, out);
   return cudaGetLastError();
 }
 
@@ -196,12 +196,16 @@ cudaError_t launch_apply_q(const T* y, T* x, int64_t n, int64_t m, const mpk::Ap
                            const mp_info* info, unsigned flags, cudaStream_t s) {
   constexpr int U = 4;
   const int t = threads_for(VEC, m);
-  const Grid g = plan_grid(VEC, n, m, pair_occupancy<T, VEC, Q>(t));
+  const void* fn = derive ? reinterpret_cast<const void*>(mpk::k_apply<T, VEC, Q, U, true>)
+                          : reinterpret_cast<const void*>(mpk::k_apply<T, VEC, Q, U, false>);
+  const Grid g = plan_grid(VEC, n, m, occupancy(fn, t));
   dim3 grid(static_cast<unsigned>(g.ntiles), static_cast<unsigned>(g.nrb));
   if (derive)
-    return launch_pdl(mpk::k_apply<T, VEC, Q, U, true>, grid, dim3(g.threads), 0, s, y, x, n, m, g.rpb, A, info,
+    return launch_pdl(mpk::k_apply<T, VEC, Q, U, true>, grid, dim3(g.threads), 0, s, y, x, n, m,
+                      kRowInterleave ? n / g.nrb : g.rpb, kRowInterleave, A, info,
                       flags);
-  return launch_pdl(mpk::k_apply<T, VEC, Q, U, false>, grid, dim3(g.threads), 0, s, y, x, n, m, g.rpb, A, info,
+  return launch_pdl(mpk::k_apply<T, VEC, Q, U, false>, grid, dim3(g.threads), 0, s, y, x, n, m,
+                      kRowInterleave ? n / g.nrb : g.rpb, kRowInterleave, A, info,
                     flags);
 }
 

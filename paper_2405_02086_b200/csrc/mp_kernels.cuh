@@ -141,32 +141,61 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // ------------------------------------------------------------------- K1
 // grid = (column tiles, row blocks); thread owns columns [c0, c0+VEC) over
 // rows [r0, r1).  out: BitsT<T>[m] (l_inf, pre-zeroed) or double[R][m].
+// Pointer step the optimiser cannot see through: without it nvcc
+// strength-reduces an unrolled p += stride into U live 64-bit addresses
+// (80 registers, occupancy 3); with it one address stays live.
+template <typename T>
+__device__ __forceinline__ T* step_ptr(T* p, int64_t elems) {
+  T* r;
+  asm("add.s64 %0, %1, %2;" : "=l"(r) : "l"(p), "l"(elems * static_cast<int64_t>(sizeof(T))));
+  return r;
+}
+
+// Row mapping shared by K1 and K3: CTA row-slot b of R walks either the
+// contiguous block [b*rpb, (b+1)*rpb) (interleave = 0) or the rows b, b+R,
+// b+2R, ... (interleave = 1: the whole grid sweeps one band of R rows at a
+// time, i.e. one contiguous ~R*m*sizeof(T) region of HBM).
+// `rpb` doubles as the interleaved quotient: with interleave the host passes
+// rpb = n / R, so slot b owns rpb + (b < n % R) rows (no device division).
+struct RowWalk {
+  int64_t r0, step, cnt;
+};
+__device__ __forceinline__ RowWalk row_walk(int64_t n, int64_t rpb, int interleave) {
+  const int64_t b = blockIdx.y, R = gridDim.y;
+  if (interleave) return {b, R, rpb + (b < n - rpb * R ? 1 : 0)};
+  const int64_t r0 = b * rpb;
+  return {r0, 1, r0 < n ? min(rpb, n - r0) : 0};
+}
+
 template <typename T, int VEC, int Q, int U>
 __global__ void __launch_bounds__(kThreads)
-    k_colnorm(const T* __restrict__ y, int64_t n, int64_t m, int64_t rpb, void* __restrict__ out) {
+    k_colnorm(const T* __restrict__ y, int64_t n, int64_t m, int64_t rpb, int interleave, void* __restrict__ out) {
   pdl_trigger();  // let the (single-CTA) outer kernel be scheduled as SMs free up
   tl_begin(0);
   const int64_t c0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * VEC;
   if (c0 >= m) return;
-  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rpb;
-  const int64_t r1 = min(n, r0 + rpb);
-  const T* p = y + r0 * m + c0;
-  int64_t r = r0;
+  const RowWalk rw = row_walk(n, rpb, interleave);
+  const int64_t ds = rw.step * m;  // element stride between consecutive rows of this CTA
+  const T* p = y + rw.r0 * m + c0;
+  int64_t k = 0;
   if constexpr (Q == kInf) {
     using B = typename BitsT<T>::type;
     B acc[VEC];
 #pragma unroll
     for (int j = 0; j < VEC; ++j) acc[j] = 0;
-    for (; r + U <= r1; r += U, p += U * m) {
+    for (; k + U <= rw.cnt; k += U) {
       T e[U][VEC];
 #pragma unroll
-      for (int u = 0; u < U; ++u) load_keep<T, VEC>(p + u * m, e[u]);
+      for (int u = 0; u < U; ++u) {  // one live address: p advances load by load
+        load_keep<T, VEC>(p, e[u]);
+        p = step_ptr(p, ds);
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int j = 0; j < VEC; ++j) acc[j] = max(acc[j], abs_bits(e[u][j]));
     }
-    for (; r < r1; ++r, p += m) {
+    for (; k < rw.cnt; ++k, p += ds) {
       T e[VEC];
       load_keep<T, VEC>(p, e);
 #pragma unroll
@@ -180,25 +209,28 @@ __global__ void __launch_bounds__(kThreads)
     double acc[VEC];
 #pragma unroll
     for (int j = 0; j < VEC; ++j) acc[j] = 0.0;
-    for (; r + U <= r1; r += U, p += U * m) {
+    for (; k + U <= rw.cnt; k += U) {
       T e[U][VEC];
 #pragma unroll
-      for (int u = 0; u < U; ++u) load_keep<T, VEC>(p + u * m, e[u]);
+      for (int u = 0; u < U; ++u) {
+        load_keep<T, VEC>(p, e[u]);
+        p = step_ptr(p, ds);
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
-          const double d = static_cast<double>(e[u][j]);
-          acc[j] = (Q == kL1) ? __dadd_rn(acc[j], fabs(d)) : __dadd_rn(acc[j], __dmul_rn(d, d));
+          const double dv = static_cast<double>(e[u][j]);
+          acc[j] = (Q == kL1) ? __dadd_rn(acc[j], fabs(dv)) : __dadd_rn(acc[j], __dmul_rn(dv, dv));
         }
     }
-    for (; r < r1; ++r, p += m) {
+    for (; k < rw.cnt; ++k, p += ds) {
       T e[VEC];
       load_keep<T, VEC>(p, e);
 #pragma unroll
       for (int j = 0; j < VEC; ++j) {
-        const double d = static_cast<double>(e[j]);
-        acc[j] = (Q == kL1) ? __dadd_rn(acc[j], fabs(d)) : __dadd_rn(acc[j], __dmul_rn(d, d));
+        const double dv = static_cast<double>(e[j]);
+        acc[j] = (Q == kL1) ? __dadd_rn(acc[j], fabs(dv)) : __dadd_rn(acc[j], __dmul_rn(dv, dv));
       }
     }
     double* part = static_cast<double*>(out) + static_cast<int64_t>(blockIdx.y) * m + c0;
@@ -812,15 +844,14 @@ __device__ __forceinline__ double load_norm(const ApplyCols& a, int64_t c) {
 // MP_FLAG_EXACT_ZERO_SIGN.
 template <typename T, int VEC, int Q, int U, bool DERIVE>
 __global__ void __launch_bounds__(kThreads)
-    k_apply(const T* __restrict__ y, T* __restrict__ x, int64_t n, int64_t m, int64_t rpb, ApplyCols A,
-            const mp_info* __restrict__ info, unsigned flags) {
+    k_apply(const T* __restrict__ y, T* __restrict__ x, int64_t n, int64_t m, int64_t rpb, int interleave,
+            ApplyCols A, const mp_info* __restrict__ info, unsigned flags) {
   pdl_wait();
   tl_begin(3);
   if (info->status != MP_OK) return;
   const int64_t c0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * VEC;
   if (c0 >= m) return;
-  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rpb;
-  const int64_t r1 = min(n, r0 + rpb);
+  const RowWalk rw = row_walk(n, rpb, interleave);
 
   // per-column parameters
   float rd[VEC], rn[VEC];
@@ -866,17 +897,18 @@ __global__ void __launch_bounds__(kThreads)
       dead = dead && (A.budgets[c0 + j] == 0.0);
     }
   }
-  if (r1 <= r0) return;
-  // Rows are swept from the END of the block backwards: K1 swept the same
-  // blocks forwards in one resident wave, so the last rows of each block are
-  // the ones still in L2 when this kernel starts.
-  const int64_t last = (r1 - 1) * m + c0;
+  if (rw.cnt <= 0) return;
+  // This CTA's rows are swept LAST-FIRST: K1 swept them first-last in the
+  // same resident wave, so the rows it touched last are still in L2 when
+  // this kernel starts.
+  const int64_t ds = rw.step * m;
+  const int64_t last = (rw.r0 + (rw.cnt - 1) * rw.step) * m + c0;
   T* q = x + last;
   if (dead) {
     T z[VEC];
 #pragma unroll
     for (int j = 0; j < VEC; ++j) z[j] = T(0);
-    for (int64_t r = r1; r > r0; --r, q -= m) store_stream<T, VEC>(q, z);
+    for (int64_t k = 0; k < rw.cnt; ++k, q -= ds) store_stream<T, VEC>(q, z);
     tl_end(3);
     return;
   }
@@ -890,19 +922,23 @@ __global__ void __launch_bounds__(kThreads)
     }
   };
   const T* p = y + last;
-  int64_t r = r1;
-  for (; r - U >= r0; r -= U, p -= U * m, q -= U * m) {
+  int64_t k = 0;
+  for (; k + U <= rw.cnt; k += U) {
     T e[U][VEC];
 #pragma unroll
-    for (int u = 0; u < U; ++u) load_last<T, VEC>(p - u * m, e[u]);
+    for (int u = 0; u < U; ++u) {  // one live address per stream
+      load_last<T, VEC>(p, e[u]);
+      p = step_ptr(p, -ds);
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
 #pragma unroll
       for (int j = 0; j < VEC; ++j) e[u][j] = op(e[u][j], j);
-      store_stream<T, VEC>(q - u * m, e[u]);
+      store_stream<T, VEC>(q, e[u]);
+      q = step_ptr(q, -ds);
     }
   }
-  for (; r > r0; --r, p -= m, q -= m) {
+  for (; k < rw.cnt; ++k, p -= ds, q -= ds) {
     T e[VEC];
     load_last<T, VEC>(p, e);
 #pragma unroll

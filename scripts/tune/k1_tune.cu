@@ -1,0 +1,85 @@
+// K1 (column max) tuning microbenchmark: times k_colnorm variants on a
+// 10000 x 10000 fp32 matrix with an L2 read-flush between launches.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -I paper_2405_02086_b200/csrc scripts/tune/k1_tune.cu -o /tmp/k1_tune
+#include <cstdio>
+#include <vector>
+
+#include "mp_kernels.cuh"
+
+__global__ void flush_read(const float4* p, size_t n, float* out) {
+  float s = 0.f;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    float4 v = __ldcs(p + i);
+    s += v.x + v.y + v.z + v.w;
+  }
+  if (s == 1234.5f) *out = s;
+}
+
+template <int VEC, int U, int IL>
+void run(const char* name, const float* y, int64_t n, int64_t m, unsigned* out, int ctas_per_sm, const float4* fl,
+         size_t fln, float* fo) {
+  auto fn = mpk::k_colnorm<float, VEC, mpk::kInf, U>;
+  int64_t slots = m / VEC;
+  int64_t tiles = (slots + 255) / 256;
+  int threads = (int)((slots + tiles - 1) / tiles);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, 0);
+  int cps = ctas_per_sm > 0 ? ctas_per_sm : occ;
+  int64_t nrb = 148LL * cps / tiles;
+  int64_t rpb = (n + nrb - 1) / nrb;
+  nrb = (n + rpb - 1) / rpb;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e9, tot = 0;
+  for (int rep = 0; rep < 12; ++rep) {
+    flush_read<<<148 * 4, 512>>>(fl, fln, fo);
+    cudaMemset(out, 0, m * 4);
+    cudaEventRecord(a);
+    fn<<<dim3(tiles, nrb), threads>>>(y, n, m, IL ? n / nrb : rpb, IL, out);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (rep >= 2) {
+      best = ms < best ? ms : best;
+      tot += ms;
+    }
+  }
+  printf("%-28s occ=%d used=%d grid=%lldx%lld thr=%d  best %.1f us  avg %.1f us  -> %.0f GB/s\n", name, occ, cps,
+         (long long)tiles, (long long)nrb, threads, best * 1e3, tot / 10 * 1e3, n * m * 4.0 / (tot / 10 * 1e-3) / 1e9);
+}
+
+int main() {
+  const int64_t n = 10000, m = 10000;
+  float* y;
+  unsigned* out;
+  cudaMalloc(&y, n * m * 4);
+  cudaMalloc(&out, m * 8);
+  std::vector<float> h(n * m);
+  for (size_t i = 0; i < h.size(); ++i) h[i] = (float)((i * 2654435761u) % 1000003) / 1000003.0f - 0.5f;
+  cudaMemcpy(y, h.data(), n * m * 4, cudaMemcpyHostToDevice);
+  size_t fln = (256ull << 20) / 16;
+  float4* fl;
+  float* fo;
+  cudaMalloc(&fl, fln * 16);
+  cudaMemset(fl, 0, fln * 16);
+  cudaMalloc(&fo, 4);
+  run<2, 16, 0>("vec2 u16 occ0 il0", y, n, m, out, 0, fl, fln, fo);
+  run<2, 8, 0>("vec2 u8 occ0 il0", y, n, m, out, 0, fl, fln, fo);
+  run<4, 8, 0>("vec4 u8 occ0 il0", y, n, m, out, 0, fl, fln, fo);
+  run<4, 4, 0>("vec4 u4 occ0 il0", y, n, m, out, 0, fl, fln, fo);
+  run<4, 16, 0>("vec4 u16 occ0 il0", y, n, m, out, 0, fl, fln, fo);
+  run<8, 4, 0>("vec8 u4 occ0 il0", y, n, m, out, 0, fl, fln, fo);
+  run<8, 2, 0>("vec8 u2 occ0 il0", y, n, m, out, 0, fl, fln, fo);
+  run<2, 16, 1>("vec2 u16 occ0 il1", y, n, m, out, 0, fl, fln, fo);
+  run<2, 8, 1>("vec2 u8 occ0 il1", y, n, m, out, 0, fl, fln, fo);
+  run<4, 8, 1>("vec4 u8 occ0 il1", y, n, m, out, 0, fl, fln, fo);
+  run<4, 4, 1>("vec4 u4 occ0 il1", y, n, m, out, 0, fl, fln, fo);
+  run<4, 16, 1>("vec4 u16 occ0 il1", y, n, m, out, 0, fl, fln, fo);
+  run<8, 4, 1>("vec8 u4 occ0 il1", y, n, m, out, 0, fl, fln, fo);
+  run<8, 2, 1>("vec8 u2 occ0 il1", y, n, m, out, 0, fl, fln, fo);
+  cudaError_t e = cudaDeviceSynchronize();
+  printf("status %s\n", cudaGetErrorString(e));
+  return 0;
+}
