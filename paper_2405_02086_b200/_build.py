@@ -18,6 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libmp_b200.so")
 DATAGEN = os.path.join(PKG, "libmp_datagen.so")
+DROPIN = os.path.join(PKG, "libmultiproj_b200.so")  # the reference C++ API over the C-ABI
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [
@@ -36,6 +37,14 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def build_cpp_test(out: str) -> str:
+    """Compile tests/cpp/dropin_test.cpp against the drop-in library."""
+    src = os.path.join(ROOT, "tests", "cpp", "dropin_test.cpp")
+    subprocess.run(["g++", "-std=c++20", "-O1", f"-I{INCLUDE}", src, f"-L{PKG}", "-lmultiproj_b200", "-lmp_b200",
+                    f"-Wl,-rpath,{PKG}", "-o", out], check=True)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> None:
     deps = glob.glob(os.path.join(CSRC, "*")) + [os.path.join(INCLUDE, "mp_cuda.h")]
     if force or _stale(LIB, deps):
@@ -45,6 +54,11 @@ def build(force: bool = False, verbose: bool = False) -> None:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
         os.replace(LIB + ".tmp", LIB)
+    di = os.path.join(CSRC, "dropin", "multiproj_dropin.cpp")
+    di_deps = [di, LIB] + glob.glob(os.path.join(INCLUDE, "multiproj", "*.hpp"))
+    if force or _stale(DROPIN, di_deps):
+        subprocess.run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", f"-I{INCLUDE}", di, f"-L{PKG}", "-lmp_b200",
+                        "-Wl,-rpath,$ORIGIN", "-o", DROPIN], check=True)
     dg = os.path.join(CSRC, "datagen.c")
     if force or _stale(DATAGEN, [dg]):
         subprocess.run(["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fPIC", "-shared", dg,
