@@ -461,6 +461,19 @@ __device__ __forceinline__ void block_sum_icount(double& s, int& c, double* sscr
   }
 }
 
+// #{j : u_j == 0 || v_j == 0} from the outer outcome (v >= 0):
+// l1 threshold -> m - |active set|; zero radius -> m; identity, l2 scale and
+// l_inf clip zero exactly the zero norms (unless the radius / scale is 0).
+__device__ __forceinline__ int outer_zero_count(int mode, int m, int active, int nzero, double eta, double scale) {
+  switch (mode) {
+    case 1: return m;
+    case 2: return m - active;
+    case 3: return scale == 0.0 ? m : nzero;
+    case 4: return eta == 0.0 ? m : nzero;
+    default: return nzero;
+  }
+}
+
 // Cluster-wide (sum, count): CTA reduction, then every thread reads the C
 // per-CTA partials through DSMEM in rank order (identical, deterministic
 // totals in every CTA).  Double-buffered partials: one cluster barrier per
@@ -521,7 +534,7 @@ __global__ void __launch_bounds__(kOuterThreads) k_outer(OuterArgs a) {
   const double eta = a.eta;
 
   double s = 0.0;
-  int bad = 0;
+  int bad = 0, nzero = 0;
 #pragma unroll
   for (int j = 0; j < P; ++j) {
     const int i = tid + j * kOuterThreads;
@@ -529,10 +542,14 @@ __global__ void __launch_bounds__(kOuterThreads) k_outer(OuterArgs a) {
       const double x = outer_load(a, base + i);
       sv[i] = x;
       bad += !isfinite(x);
+      nzero += (x == 0.0);
       s += (a.p == kL2) ? x * x : fabs(x);
     }
   }
-  cluster_sum_icount(s, bad, sscr, cscr, cps, cpc, par, cl, C);
+  int flags_zeros = ((bad > 0) << 18) + nzero;
+  cluster_sum_icount(s, flags_zeros, sscr, cscr, cps, cpc, par, cl, C);
+  bad = flags_zeros >> 18;
+  nzero = flags_zeros & ((1 << 18) - 1);
   if (bad) {
     if (rank == 0 && tid == 0) {
       a.info->status = MP_ERR_VALUE;
@@ -599,56 +616,39 @@ __global__ void __launch_bounds__(kOuterThreads) k_outer(OuterArgs a) {
   }
 
   if (rank == 0 && tid == 0) outer_publish(a, mode, tau, scale);
-  double zs = 0.0;  // zero-column count (exact in f64)
-  int surv = 0;
-  if (a.emit) {
   double* __restrict__ uo = a.u_out + base;
-#pragma unroll
-  for (int j = 0; j < P; ++j) {
-    const int i = tid + j * kOuterThreads;
-    if (i < cnt) {
-      const double x = sv[i];
-      double u = x;
-      if (mode == 2) {
-        const double dd = fabs(x) - tau;
-        u = dd > 0.0 ? copysign(dd, x) : 0.0;
-      } else if (mode == 4) {
-        u = fabs(x) > eta ? copysign(eta, x) : x;
-      } else if (mode == 3) {
-        u = x * scale;
-      } else if (mode == 1) {
-        u = 0.0;
-      }
-      uo[i] = u;
-      zs += (u == 0.0 || x == 0.0) ? 1.0 : 0.0;
-      surv += (u != 0.0);
-      sv[i] = u;  // keep u for the optional side outputs below
-    }
-  }
-  if (a.v_out || a.rdrn || a.factor) {
+  if (a.emit) {
 #pragma unroll
     for (int j = 0; j < P; ++j) {
       const int i = tid + j * kOuterThreads;
       if (i < cnt) {
-        const double u = sv[i];
-        if (a.rdrn) a.rdrn[base + i] = make_float2(__double2float_rz(u), __double2float_rn(u));
-        if (a.v_out || a.factor) {
-          const double x = outer_load(a, base + i);
-          if (a.v_out) a.v_out[base + i] = x;
-          if (a.factor) a.factor[base + i] = (x > u) ? u / x : 1.0;
+        const double x = sv[i];
+        double u = x;
+        if (mode == 2) {
+          const double dd = fabs(x) - tau;
+          u = dd > 0.0 ? copysign(dd, x) : 0.0;
+        } else if (mode == 4) {
+          u = fabs(x) > eta ? copysign(eta, x) : x;
+        } else if (mode == 3) {
+          u = x * scale;
+        } else if (mode == 1) {
+          u = 0.0;
         }
+        uo[i] = u;
+        if (a.rdrn) a.rdrn[base + i] = make_float2(__double2float_rz(u), __double2float_rn(u));
+        if (a.v_out) a.v_out[base + i] = x;
+        if (a.factor) a.factor[base + i] = (x > u) ? u / x : 1.0;
       }
     }
   }
-  }
-  cluster_sum_icount(zs, surv, sscr, cscr, cps, cpc, par, cl, C);
+  const int zeros = outer_zero_count(mode, m, active, nzero, eta, scale);
   if (rank == 0 && tid == 0) {
     a.info->status = MP_OK;
     a.info->tau = tau;
     a.info->active = active;
     a.info->iterations = iters;
-    a.info->zero_columns = static_cast<long long>(zs);
-    a.info->survivors = surv;
+    a.info->zero_columns = zeros;
+    a.info->survivors = m - zeros;
   }
   cl.sync();  // no CTA leaves while a peer may still read its DSMEM
   tl_end(2);
@@ -708,12 +708,18 @@ __global__ void __launch_bounds__(kOuterRegThreads, 1) k_outer_reg(OuterArgs a) 
     const int i = tid + j * kOuterRegThreads;
     v[j] = (i < m) ? outer_load(a, i) : 0.0;
   }
+  int nzero = 0;
 #pragma unroll
   for (int j = 0; j < P; ++j) {
     bad += !isfinite(v[j]);
+    nzero += (v[j] == 0.0) && (tid + j * kOuterRegThreads < m);
     s += (a.p == kL2) ? v[j] * v[j] : fabs(v[j]);
   }
-  block_allreduce(s, bad, sb, cb, par);
+  // one int channel: non-finite flag (bit 18+) and #{v == 0} (bits 0..17)
+  int flags_zeros = ((bad > 0) << 18) + nzero;
+  block_allreduce(s, flags_zeros, sb, cb, par);
+  bad = flags_zeros >> 18;
+  nzero = flags_zeros & ((1 << 18) - 1);
   if (bad) {
     if (tid == 0) {
       a.info->status = MP_ERR_VALUE;
@@ -775,8 +781,9 @@ __global__ void __launch_bounds__(kOuterRegThreads, 1) k_outer_reg(OuterArgs a) 
   }
 
   if (tid == 0) outer_publish(a, mode, tau, scale);
-  double zs = 0.0;
-  int surv = 0;
+  // Zero columns follow from the outcome (u == 0 <=> v <= tau for the l1
+  // threshold, v == 0 for identity / scale / clip); survivors = m - zeros.
+  const int zeros = outer_zero_count(mode, m, active, nzero, eta, scale);
   if (a.emit) {
 #pragma unroll
     for (int j = 0; j < P; ++j) {
@@ -798,19 +805,16 @@ __global__ void __launch_bounds__(kOuterRegThreads, 1) k_outer_reg(OuterArgs a) 
         if (a.v_out) a.v_out[i] = x;
         if (a.rdrn) a.rdrn[i] = make_float2(__double2float_rz(u), __double2float_rn(u));
         if (a.factor) a.factor[i] = (x > u) ? u / x : 1.0;
-        zs += (u == 0.0 || x == 0.0) ? 1.0 : 0.0;
-        surv += (u != 0.0);
       }
     }
-    block_allreduce(zs, surv, sb, cb, par);
   }
   if (tid == 0) {
     a.info->status = MP_OK;
     a.info->tau = tau;
     a.info->active = active;
     a.info->iterations = iters;
-    a.info->zero_columns = static_cast<long long>(zs);  // emit = 0: the apply pass accumulates them
-    a.info->survivors = surv;
+    a.info->zero_columns = zeros;
+    a.info->survivors = m - zeros;
   }
   tl_end(2);
 }
@@ -820,7 +824,7 @@ __global__ void __launch_bounds__(kOuterRegThreads, 1) k_outer_reg(OuterArgs a) 
 // thread derives its columns' budgets from the norms and K2's OuterParams --
 // u = derive_u(P, v) -- so K2 stays a short serial step and the per-column
 // work is spread over the whole grid; row block 0 also writes the user-facing
-// budgets / norms and accumulates zero_columns / survivors.  Otherwise
+// budgets / norms (K2 already counted zero_columns / survivors).  Otherwise
 // (multi-level levels): precomputed colp (float2 {RD(u), RN(u)} for f32
 // l_inf, double u for f64 l_inf, double factor for l2) and budgets.
 struct ApplyCols {
@@ -831,7 +835,7 @@ struct ApplyCols {
   const OuterParams* params;
   double* u_out;          // DERIVE, nullable
   double* v_out;          // DERIVE, nullable
-  mp_info* info_w;        // DERIVE: zero_columns / survivors accumulators
+  mp_info* info_w;        // unused (K2 counts zero columns); kept for ABI of the kernel args
 };
 
 __device__ __forceinline__ double load_norm(const ApplyCols& a, int64_t c) {
@@ -859,7 +863,6 @@ __global__ void __launch_bounds__(kThreads)
   bool dead = !(flags & MP_FLAG_EXACT_ZERO_SIGN);
   if constexpr (DERIVE) {
     const OuterParams P = *A.params;
-    unsigned long long zc = 0, sv = 0;
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
       const double vj = load_norm(A, c0 + j);
@@ -876,13 +879,7 @@ __global__ void __launch_bounds__(kThreads)
       if (blockIdx.y == 0) {
         if (A.u_out) A.u_out[c0 + j] = uj;
         if (A.v_out) A.v_out[c0 + j] = vj;
-        zc += (uj == 0.0 || vj == 0.0);
-        sv += (uj != 0.0);
       }
-    }
-    if (blockIdx.y == 0) {
-      if (zc) atomicAdd(reinterpret_cast<unsigned long long*>(&A.info_w->zero_columns), zc);
-      if (sv) atomicAdd(reinterpret_cast<unsigned long long*>(&A.info_w->survivors), sv);
     }
   } else {
 #pragma unroll

@@ -255,12 +255,14 @@ inline int cols_stride(int64_t n) {
   return static_cast<int>(((n + 3) / 4) * 4 + 4);  // 16-byte aligned columns, offset banks
 }
 
+constexpr int kColsTW = 2;  // warps per column (occupancy is bounded by shared memory)
+
 template <typename T, int W>
 cudaError_t cols_attr() {
-  cudaError_t e = cudaFuncSetAttribute(k_l1cols<T, W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(k_l1cols<T, W, kColsTW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(kColsSmemMax));
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_l1cols<T, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(k_l1cols<T, W, kColsTW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(kColsSmemMax));
 }
 
@@ -286,7 +288,7 @@ cudaError_t launch_cols(const T* y, T* x, int64_t n, int64_t m, const double* v,
   const size_t smem = static_cast<size_t>(W) * stride * sizeof(T);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>((m + W - 1) / W));
-  cfg.blockDim = dim3(32 * W);
+  cfg.blockDim = dim3(32 * W * kColsTW);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -295,9 +297,9 @@ cudaError_t launch_cols(const T* y, T* x, int64_t n, int64_t m, const double* v,
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (dv.params)
-    return cudaLaunchKernelEx(&cfg, k_l1cols<T, W, true>, y, x, static_cast<int>(n), m, stride, v, u, ws.tau, info,
+    return cudaLaunchKernelEx(&cfg, k_l1cols<T, W, kColsTW, true>, y, x, static_cast<int>(n), m, stride, v, u, ws.tau, info,
                               dv.params, dv.u_out, dv.info_w);
-  return cudaLaunchKernelEx(&cfg, k_l1cols<T, W, false>, y, x, static_cast<int>(n), m, stride, v, u, ws.tau, info,
+  return cudaLaunchKernelEx(&cfg, k_l1cols<T, W, kColsTW, false>, y, x, static_cast<int>(n), m, stride, v, u, ws.tau, info,
                             dv.params, dv.u_out, dv.info_w);
 }
 

@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kLargeThreads) k_outer_large(OuterArgs a, Larg
 
   if (b == 0 && threadIdx.x == 0) outer_publish(a, mode, tau, scale);
   long long zeros = 0, surv = 0;
-  for (int64_t i = i0 + threadIdx.x; i < i1 && a.emit; i += blockDim.x) {
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     const double x = outer_load(a, i);
     double u;
     switch (mode) {
@@ -182,10 +182,11 @@ __global__ void __launch_bounds__(kLargeThreads) k_outer_large(OuterArgs a, Larg
       case 4: u = fabs(x) > eta ? copysign(eta, x) : x; break;
       default: u = x;
     }
-    a.u_out[i] = u;
-    if (a.v_out) a.v_out[i] = x;
     zeros += (u == 0.0 || x == 0.0);
     surv += (u != 0.0);
+    if (!a.emit) continue;
+    a.u_out[i] = u;
+    if (a.v_out) a.v_out[i] = x;
     if (a.rdrn) a.rdrn[i] = make_float2(__double2float_rz(u), __double2float_rn(u));
     if (a.factor) a.factor[i] = (x > u) ? u / x : 1.0;
   }

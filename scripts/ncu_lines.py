@@ -13,22 +13,23 @@ rows = list(csv.reader(io.StringIO(out)))
 hdr = None
 agg = {}
 seen_fn = 0
+fname = "?"
 for r in rows:
-    if r and r[0] == "Function Name":
-        seen_fn += 1
-        if seen_fn > 1:
-            break
+    if r and r[0] in ("File Path", "File Name"):
+        fname = r[1].split("/")[-1]
+        continue
     if r and r[0] == "Line No":
         hdr = r
         continue
     if hdr and len(r) == len(hdr) and r[0].isdigit():
         ie = int(r[hdr.index("Instructions Executed")] or 0)
         ws = int(r[hdr.index("Warp Stall Sampling (All Samples)")] or 0)
-        a = agg.setdefault(int(r[0]), [0, 0, r[1]])
+        a = agg.setdefault((fname, int(r[0])), [0, 0, r[1]])
         a[0] += ie
         a[1] += ws
 tot_i = sum(v[0] for v in agg.values())
 tot_s = sum(v[1] for v in agg.values())
 print(f"total instructions {tot_i}, samples {tot_s}")
-for ln, (ie, ws, src) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
-    print(f"{ln:5d} {ie:8d} {ws:5d}  {src.strip()[:90]}")
+print("-- by stall samples")
+for (fn, ln), (ie, ws, src) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
+    print(f"{fn[:14]:14s}{ln:5d} {ie:9d} {ws:6d}  {src.strip()[:80]}")

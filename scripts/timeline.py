@@ -21,7 +21,7 @@ x = torch.empty_like(y)
 colmax = np.abs(y_h).max(axis=0).astype(np.float64)
 p = mp.BilevelProjector(n, m, "float32", "1", q)
 flush_buf = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
-tl = torch.empty(8, dtype=torch.int64, device="cuda")
+tl = torch.empty(16, dtype=torch.int64, device="cuda")
 s = torch.cuda.Stream()
 for rel in [float(r) for r in os.environ.get("RELS", "0.001,0.5").split(",")]:
     eta = rel * float(colmax.sum()) if q == "inf" else rel * float(np.abs(y_h).astype(np.float64).sum())
@@ -33,7 +33,7 @@ for rel in [float(r) for r in os.environ.get("RELS", "0.001,0.5").split(",")]:
             p(y, x, eta, stream=s)
     res = []
     for rep in range(20):
-        init = torch.tensor([2**63 - 1, 0] * 4, dtype=torch.int64, device="cuda")
+        init = torch.tensor([2**63 - 1, 0] * 4 + [0] * 8, dtype=torch.int64, device="cuda")
         tl.copy_(init)
         L.mp_profile_timeline(tl.data_ptr())
         with torch.cuda.stream(s):
@@ -48,6 +48,9 @@ for rel in [float(r) for r in os.environ.get("RELS", "0.001,0.5").split(",")]:
         t0 = t[0]
         rel_t = [(t[i] - t0) / 1e3 if t[i] not in (0, 2**63 - 1) else float("nan") for i in range(8)]
         res.append(rel_t + [e0.elapsed_time(e1) * 1e3])
+        extra = t[8:11]
+    if extra[2] > 0:
+        print(f"  l1 inner passes: mean {extra[0] / extra[2]:.2f} max {extra[1]:.0f} over {extra[2]:.0f} columns")
     inf_ = p.info()
     print(f"  info: iterations={inf_.iterations} survivors={inf_.survivors} zero_columns={inf_.zero_columns}")
     r = np.median(np.array(res), axis=0)
