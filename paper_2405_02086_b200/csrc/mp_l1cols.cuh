@@ -178,6 +178,8 @@ __global__ void __launch_bounds__(32 * W * TW)
                       (reinterpret_cast<uintptr_t>(y + c0) % 16) == 0 &&
                       (reinterpret_cast<uintptr_t>(x + c0) % 16) == 0;
 
+  const long long ck0 = clock64();
+  long long ck1 = ck0, ck2 = ck0;
   if (any_proj) {
     // ---- stage |y| (16-byte pieces, 8 in flight per thread)
     if (vec_ok) {
@@ -229,6 +231,7 @@ __global__ void __launch_bounds__(32 * W * TW)
       }
     }
     __syncthreads();
+    ck1 = clock64();
 
     // ---- per-column Michelot with per-thread active-set compaction
     if (kind == 3) {
@@ -261,6 +264,7 @@ __global__ void __launch_bounds__(32 * W * TW)
     }
     __syncthreads();
   }
+  ck2 = clock64();
   if (cl == 0 && colok) tau_out[col] = stau[w];
 
   // ---- apply: re-read y (L2), write x in 16-byte row pieces
@@ -330,6 +334,12 @@ __global__ void __launch_bounds__(32 * W * TW)
         __stcs(reinterpret_cast<float4*>(dst), make_float4(vals[0], vals[1 % kPer16], vals[2 % kPer16], vals[3 % kPer16]));
       else
         __stcs(reinterpret_cast<double2*>(dst), make_double2(vals[0], vals[1 % kPer16]));
+    }
+    if (threadIdx.x == 0 && g_mp_timeline) {  // profiling aid: per-phase SM cycles in slots 11..13
+      const long long ck3 = clock64();
+      atomicAdd(g_mp_timeline + 11, static_cast<unsigned long long>(ck1 - ck0));
+      atomicAdd(g_mp_timeline + 12, static_cast<unsigned long long>(ck2 - ck1));
+      atomicAdd(g_mp_timeline + 13, static_cast<unsigned long long>(ck3 - ck2));
     }
   } else {
     for (int idx = threadIdx.x; idx < n * W; idx += NT) {

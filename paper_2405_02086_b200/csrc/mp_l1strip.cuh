@@ -28,6 +28,7 @@
 #include "mp_internal.h"
 #include "mp_kernels.cuh"
 #include "mp_l1cols.cuh"
+#include "mp_l1quad.cuh"
 
 namespace mpk {
 
@@ -273,8 +274,17 @@ struct L1Derive {
   mp_info* info_w = nullptr;
 };
 
+template <typename T>
+cudaError_t quad_attr() {
+  cudaError_t e = cudaFuncSetAttribute(k_l1quad<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kColsSmemMax));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_l1quad<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(kColsSmemMax));
+}
+
 inline cudaError_t l1strip_setup() {
-  for (cudaError_t e : {cols_attr<float, 8>(), cols_attr<float, 4>(), cols_attr<float, 2>(), cols_attr<float, 1>(),
+  for (cudaError_t e : {quad_attr<float>(), quad_attr<double>(), cols_attr<float, 8>(), cols_attr<float, 4>(), cols_attr<float, 2>(), cols_attr<float, 1>(),
                         cols_attr<double, 8>(), cols_attr<double, 4>(), cols_attr<double, 2>(),
                         cols_attr<double, 1>()})
     if (e != cudaSuccess) return e;
@@ -317,6 +327,23 @@ template <typename T>
 cudaError_t launch_l1strip(const T* y, T* x, int64_t n, int64_t m, const double* v, const double* u,
                            const L1StripWs& ws, const mp_info* info, unsigned flags, cudaStream_t s,
                            const L1Derive& dv = L1Derive()) {
+  if (l1_quad_ok<T>(y, x, m) && static_cast<size_t>(n) * 16 <= kColsSmemMax) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(m / (16 / sizeof(T))));
+    cfg.blockDim = dim3(kQuadThreads);
+    cfg.dynamicSmemBytes = static_cast<size_t>(n) * 16;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (dv.params)
+      return cudaLaunchKernelEx(&cfg, k_l1quad<T, true>, y, x, static_cast<int>(n), m, v, u, ws.tau, info, dv.params,
+                                dv.u_out);
+    return cudaLaunchKernelEx(&cfg, k_l1quad<T, false>, y, x, static_cast<int>(n), m, v, u, ws.tau, info, dv.params,
+                              dv.u_out);
+  }
   const size_t col_bytes = static_cast<size_t>(cols_stride<T>(n)) * sizeof(T);
   if (8 * col_bytes <= kColsSmemTarget) return launch_cols<T, 8>(y, x, n, m, v, u, ws, info, dv, s);
   if (4 * col_bytes <= kColsSmemTarget) return launch_cols<T, 4>(y, x, n, m, v, u, ws, info, dv, s);
