@@ -126,6 +126,13 @@ size_t mp_aggregate_workspace_size(mp_dtype dtype, int64_t n, int64_t m, mp_norm
 mp_status mp_aggregate(const void* t, double* out, mp_dtype dtype, int64_t n, int64_t m,
                        mp_norm q, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Config-5 workload harness (BASELINE.json config 5, the per-step
+ * projection of proj/src/train.cpp:191-199): x += sigma * N(0, 1), with the
+ * deviates from Philox4x32-10 keyed by (seed, iteration) on the element
+ * index -- stateless, graph-replayable, reproducible. */
+mp_status mp_perturb_gaussian(void* x, mp_dtype dtype, int64_t count, double sigma, uint64_t seed,
+                              uint64_t iteration, void* stream);
+
 /* ------------------------------------------------------------------ host */
 
 /* Opaque per-thread-safe execution context: device, stream, cached device
@@ -157,7 +164,8 @@ mp_status mp_aggregate_host(mp_context* ctx, const void* t, double* out, mp_dtyp
 /* ----------------------------------------------------------- diagnostics */
 
 /* Per-phase device timing (bench / profiling aid, not in the reference):
- * while set, every mp_bilevel_project call on this host thread records
+ * while set, every mp_bilevel_project / mp_multilevel_project call on this
+ * host thread records
  * events[0..3] (cudaEvent_t) on its stream before the norm pass, after the
  * norm pass, after the outer projection and after the apply pass.  Recorded
  * events are stream-ordered, so they work inside CUDA-graph capture.  Pass

@@ -26,7 +26,7 @@ from ._capi import (MP_F32, MP_F64, MP_FLAG_EXACT_ZERO_SIGN, MpInfo, MpConfigErr
 __all__ = [
     "bilevel_project", "multilevel_project", "trilevel_project_l1infinf", "project_l1", "project_l2",
     "project_linf", "project_ball", "matrix_pq_norm", "multilevel_norm", "aggregate_leading_axis",
-    "structured_sparsity", "gen_uniform_matrix", "BilevelProjector", "MultilevelProjector",
+    "structured_sparsity", "gen_uniform_matrix", "perturb_gaussian", "BilevelProjector", "MultilevelProjector",
     "ProjectionError", "MpValueError", "MpShapeError", "MpConfigError", "MP_FLAG_EXACT_ZERO_SIGN",
 ]
 
@@ -286,6 +286,16 @@ def structured_sparsity(y, tol=0.0):
     mx = aggregate_leading_axis(arr, "inf")
     count = int(np.sum(mx <= tol))
     return count, count / arr.shape[1]
+
+
+def perturb_gaussian(x, sigma, seed, iteration, stream=None):
+    """In-place x += sigma * N(0,1) on a torch CUDA tensor (config-5 loop
+    harness; Philox4x32-10 keyed by (seed, iteration))."""
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    check(lib().mp_perturb_gaussian(x.data_ptr(), _dt(x), x.numel(), float(sigma), int(seed), int(iteration),
+                                    s.cuda_stream))
+    return x
 
 
 def gen_uniform_matrix(n, m, seed, lo=0.0, hi=1.0):

@@ -23,7 +23,7 @@ EXPORTS = [
     "mp_aggregate_workspace_size", "mp_aggregate",
     "mp_context_create", "mp_context_destroy",
     "mp_bilevel_project_host", "mp_multilevel_project_host",
-    "mp_project_ball_host", "mp_aggregate_host",
+    "mp_project_ball_host", "mp_aggregate_host", "mp_perturb_gaussian",
     "mp_profile_events", "mp_profile_timeline", "mp_last_error", "mp_version",
 ]
 
@@ -97,6 +97,8 @@ def lib() -> C.CDLL:
     L.mp_aggregate_host.restype = st
     L.mp_profile_events.argtypes = [C.c_void_p, C.c_int]
     L.mp_profile_events.restype = None
+    L.mp_perturb_gaussian.argtypes = [vp, en, i64, dbl, C.c_uint64, C.c_uint64, vp]
+    L.mp_perturb_gaussian.restype = st
     L.mp_profile_timeline.argtypes = [C.c_void_p]
     L.mp_profile_timeline.restype = None
     L.mp_last_error.argtypes = []

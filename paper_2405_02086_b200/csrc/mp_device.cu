@@ -14,6 +14,7 @@
 #include "mp_kernels.cuh"
 #include "mp_l1strip.cuh"
 #include "mp_outer_large.cuh"
+#include "mp_perturb.cuh"
 
 namespace mpi {
 
@@ -579,7 +580,12 @@ mp_status multilevel_impl(const T* t, T* x, mp_dtype dt, const int64_t* shape, i
   MultiWs w = carve_multi(c, dt, shape, order, levels);
   if (!c.fits()) return fail(MP_ERR_WORKSPACE, "mp_multilevel_project: workspace too small");
   MP_CUDA_TRY(outer_setup());
-  if (order == 1) return vector_impl(t, x, dt, shape[0], levels[0], eta, info, w.vec, s);
+  prof_mark(0, s);
+  if (order == 1) {
+    mp_status st1 = vector_impl(t, x, dt, shape[0], levels[0], eta, info, w.vec, s);
+    prof_mark(3, s);
+    return st1;
+  }
 
   std::vector<int64_t> M(order + 1, 1);
   for (int i = order - 1; i >= 0; --i) M[i] = M[i + 1] * shape[i];
@@ -624,6 +630,7 @@ mp_status multilevel_impl(const T* t, T* x, mp_dtype dt, const int64_t* shape, i
   }
   MP_CUDA_TRY(launch_colparams<T>(w.agg[1], B[1], M[1], levels[0], w.colp, inf, s));
   MP_CUDA_TRY(project_fibers<T>(t, x, shape[0], M[1], levels[0], w.agg[1], B[1], w.colp, w.l1, inf, flags, dt, s));
+  prof_mark(3, s);
   return MP_OK;
 }
 
@@ -705,6 +712,32 @@ mp_status mp_multilevel_project(const void* t, void* x, mp_dtype dtype, const in
                                   eta, budget_chain, info, flags, workspace, workspace_bytes, s);
   return multilevel_impl<double>(static_cast<const double*>(t), static_cast<double*>(x), dtype, shape, order, levels,
                                  eta, budget_chain, info, flags, workspace, workspace_bytes, s);
+}
+
+mp_status mp_perturb_gaussian(void* x, mp_dtype dtype, int64_t count, double sigma, uint64_t seed, uint64_t iteration,
+                              void* stream) {
+  if (!dtype_ok(dtype)) return fail(MP_ERR_CONFIG, "unknown dtype code");
+  if (count < 0 || (count > 0 && !x)) return fail(MP_ERR_SHAPE, "bad tensor");
+  if (!(sigma >= 0.0) || !std::isfinite(sigma)) return fail(MP_ERR_VALUE, "sigma must be a finite nonnegative real");
+  if (count == 0) return MP_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t quads = (count + 3) / 4;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((quads + 255) / 256, sm_count() * 8));
+  const uint32_t lo = static_cast<uint32_t>(seed), hi = static_cast<uint32_t>(seed >> 32);
+  const uint32_t it = static_cast<uint32_t>(iteration);
+  if (dtype == MP_F32) {
+    if (count % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0)
+      mpk::k_perturb_gaussian<float, true><<<blocks, 256, 0, s>>>(static_cast<float*>(x), count,
+                                                                  static_cast<float>(sigma), lo, hi, it);
+    else
+      mpk::k_perturb_gaussian<float, false><<<blocks, 256, 0, s>>>(static_cast<float*>(x), count,
+                                                                   static_cast<float>(sigma), lo, hi, it);
+  } else {
+    mpk::k_perturb_gaussian<double, false><<<blocks, 256, 0, s>>>(static_cast<double*>(x), count,
+                                                                  static_cast<float>(sigma), lo, hi, it);
+  }
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
 }
 
 size_t mp_project_ball_workspace_size(mp_dtype dtype, int64_t len, mp_norm q) {
