@@ -97,8 +97,9 @@ class BilevelProjector:
 class MultilevelProjector:
     """Pre-planned multi-level projection on device tensors (graph capturable)."""
 
-    def __init__(self, shape, levels, dtype="float32", device=None, flags: int = 0):
+    def __init__(self, shape, levels, dtype="float32", device=None, flags: int = 0, want_chain: bool = True):
         import torch
+        self.want_chain = want_chain  # False lets (inf, ..., inf, p) specs collapse to one bi-level pass
         self.shape = [int(s) for s in shape]
         self.levels = parse_norm_spec(levels)
         self.tdtype = torch.float32 if str(dtype) in ("float32", "torch.float32") else torch.float64
@@ -124,7 +125,8 @@ class MultilevelProjector:
         import torch
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         check(lib().mp_multilevel_project(t.data_ptr(), x.data_ptr(), self.dt, self._shape_c, len(self.shape),
-                                          self._lv_c, len(self.levels), float(eta), self.chain.data_ptr(),
+                                          self._lv_c, len(self.levels), float(eta),
+                                          self.chain.data_ptr() if self.want_chain else None,
                                           self.info_buf.data_ptr(), self.flags, self.ws.data_ptr(),
                                           self.ws.numel(), s.cuda_stream))
         return x
@@ -193,7 +195,8 @@ def multilevel_project(y, norms, eta, workers=1, flags: int = 0, return_chain: b
     sizes = [int(np.prod(arr.shape[i:])) for i in range(arr.ndim - 1, 0, -1)]
     chain = np.empty(max(1, sum(sizes)), np.float64)
     check(lib().mp_multilevel_project_host(None, arr.ctypes.data, x.ctypes.data, _dt(arr), shape, arr.ndim, lv,
-                                           len(levels), float(eta), chain.ctypes.data, flags))
+                                           len(levels), float(eta), chain.ctypes.data if return_chain else None,
+                                           flags))
     if not return_chain:
         return x
     out, off = [], 0

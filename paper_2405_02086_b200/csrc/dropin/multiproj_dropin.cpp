@@ -199,7 +199,11 @@ NormSpec parse_norm_spec(const std::string& s) {
   }
 }
 
-MultilevelResult multilevel_project_iter(const DenseTensor& t, const NormSpec& nu, double eta, ThreadPool* /*pool*/) {
+namespace {
+
+// want_chain = false lets the device take the collapsed (inf, ..., inf, p)
+// path; the projected tensor is the same bit for bit.
+MultilevelResult run_multilevel(const DenseTensor& t, const NormSpec& nu, double eta, bool want_chain) {
   if (nu.depth() == 0) throw ConfigError("empty norm spec");
   if (nu.depth() != t.order()) throw ShapeError("norm spec depth does not match tensor order");
   check_radius(eta);
@@ -214,8 +218,9 @@ MultilevelResult multilevel_project_iter(const DenseTensor& t, const NormSpec& n
   }
   std::vector<double> x(t.size()), chain(std::max<std::size_t>(chain_len, 1));
   check(mp_multilevel_project_host(nullptr, t.data().data(), x.data(), MP_F64, shape.data(), order, levels.data(),
-                                   order, eta, chain.data(), MP_FLAG_EXACT_ZERO_SIGN));
+                                   order, eta, want_chain ? chain.data() : nullptr, MP_FLAG_EXACT_ZERO_SIGN));
   MultilevelResult r{DenseTensor(t.shape(), x), {}};
+  if (!want_chain) return r;
   std::size_t off = 0;
   for (int i = order - 1; i >= 1; --i) {
     std::vector<std::size_t> sh(t.shape().begin() + i, t.shape().end());
@@ -228,15 +233,21 @@ MultilevelResult multilevel_project_iter(const DenseTensor& t, const NormSpec& n
   return r;
 }
 
-DenseTensor multilevel_project(const DenseTensor& t, const NormSpec& nu, double eta, ThreadPool* pool) {
-  // The recursive and iterative forms agree bit for bit in the reference
-  // (proj/tests/test_multilevel.cpp:44-67); one device algorithm serves both.
-  return multilevel_project_iter(t, nu, eta, pool).X;
+}  // namespace
+
+MultilevelResult multilevel_project_iter(const DenseTensor& t, const NormSpec& nu, double eta, ThreadPool* /*pool*/) {
+  return run_multilevel(t, nu, eta, true);
 }
 
-DenseTensor trilevel_project_l1infinf(const DenseTensor& t, double eta, ThreadPool* pool) {
+DenseTensor multilevel_project(const DenseTensor& t, const NormSpec& nu, double eta, ThreadPool* /*pool*/) {
+  // The recursive and iterative forms agree bit for bit in the reference
+  // (proj/tests/test_multilevel.cpp:44-67); one device algorithm serves both.
+  return run_multilevel(t, nu, eta, false).X;
+}
+
+DenseTensor trilevel_project_l1infinf(const DenseTensor& t, double eta, ThreadPool* /*pool*/) {
   if (t.order() != 3) throw ShapeError("trilevel_project_l1infinf requires order 3");
-  return multilevel_project_iter(t, NormSpec{{Norm::Inf, Norm::Inf, Norm::L1}}, eta, pool).X;
+  return run_multilevel(t, NormSpec{{Norm::Inf, Norm::Inf, Norm::L1}}, eta, false).X;
 }
 
 double multilevel_norm(const DenseTensor& t, const NormSpec& nu) {
@@ -300,7 +311,7 @@ DenseTensor run_projection(const Algorithm& a, const DenseTensor& input, double 
     case Algorithm::Kind::BilevelL1Inf: return bilevel_project(input, Norm::L1, Norm::Inf, eta, pool).X;
     case Algorithm::Kind::BilevelL11: return bilevel_project(input, Norm::L1, Norm::L1, eta, pool).X;
     case Algorithm::Kind::BilevelL12: return bilevel_project(input, Norm::L1, Norm::L2, eta, pool).X;
-    case Algorithm::Kind::Multilevel: return multilevel_project_iter(input, a.spec, eta, pool).X;
+    case Algorithm::Kind::Multilevel: return multilevel_project(input, a.spec, eta, pool);
     case Algorithm::Kind::Euclid:
       throw ConfigError("'euclid' (exact Euclidean l1,inf) is not part of the B200 bi-level drop-in");
   }

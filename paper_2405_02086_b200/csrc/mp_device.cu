@@ -163,15 +163,32 @@ int64_t max_nrb(mp_dtype dt, int64_t n, int64_t m) {
 // interleaved across the grid (kRowInterleave), so both kernels sweep HBM
 // band by band and K3's reverse sweep starts on the bands K1 read last --
 // still in L2 -- whatever the two grids are.
+// Row groups per K1 CTA: narrow matrices stack row groups (up to 1024
+// threads) so each column gets one atomic / partial per CTA.
+inline int k1_row_groups(int tx) { return tx >= 128 ? 1 : std::min(16, 1024 / tx); }
+
+template <typename T, int VEC, int Q, bool RG>
+cudaError_t launch_colnorm_rg(int64_t n, int64_t m, const T* y, void* out, Grid& g, cudaStream_t s) {
+  constexpr int U = (sizeof(T) * VEC == 32) ? 4 : 8;  // 128 bytes of loads in flight per thread
+  auto fn = mpk::k_colnorm<T, VEC, Q, U, RG>;
+  const int tx = threads_for(VEC, m);
+  const int ty = RG ? k1_row_groups(tx) : 1;
+  const size_t smem = ty > 1 ? static_cast<size_t>(ty) * tx * VEC * 8 : 0;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessorWithFlags(&occ, fn, tx * ty, smem, 0) != cudaSuccess || occ < 1)
+    occ = 1;
+  g = plan_grid(VEC, n, m, occ);  // g.nrb = CTA rows; row slots = g.nrb * ty
+  const int64_t slots = g.nrb * ty;
+  const int64_t rpb = kRowInterleave ? n / slots : (n + slots - 1) / slots;
+  dim3 grid(static_cast<unsigned>(g.ntiles), static_cast<unsigned>(g.nrb));
+  fn<<<grid, dim3(tx, ty), smem, s>>>(y, n, m, rpb, kRowInterleave, out);
+  return cudaGetLastError();
+}
+
 template <typename T, int VEC, int Q>
 cudaError_t launch_colnorm_q(int64_t n, int64_t m, const T* y, void* out, Grid& g, cudaStream_t s) {
-  constexpr int U = (sizeof(T) * VEC == 32) ? 4 : 8;  // 128 bytes of loads in flight per thread
-  auto fn = mpk::k_colnorm<T, VEC, Q, U>;
-  const int t = threads_for(VEC, m);
-  g = plan_grid(VEC, n, m, occupancy(reinterpret_cast<const void*>(fn), t));
-  dim3 grid(static_cast<unsigned>(g.ntiles), static_cast<unsigned>(g.nrb));
-  fn<<<grid, g.threads, 0, s>>>(y, n, m, kRowInterleave ? n / g.nrb : g.rpb, kRowInterleave, out);
-  return cudaGetLastError();
+  if (k1_row_groups(threads_for(VEC, m)) > 1) return launch_colnorm_rg<T, VEC, Q, true>(n, m, y, out, g, s);
+  return launch_colnorm_rg<T, VEC, Q, false>(n, m, y, out, g, s);
 }
 
 template <typename T, int VEC>
@@ -634,6 +651,17 @@ mp_status multilevel_impl(const T* t, T* x, mp_dtype dt, const int64_t* shape, i
   return MP_OK;
 }
 
+// Specs whose inner levels are all l_inf (order >= 2); rows = d0*...*d_{r-2}.
+bool inf_inner_levels(const int64_t* shape, int order, const mp_norm* levels, int64_t& rows) {
+  if (order < 2) return false;
+  rows = 1;
+  for (int i = 0; i + 1 < order; ++i) {
+    if (levels[i] != MP_NORM_INF) return false;
+    rows *= shape[i];
+  }
+  return true;
+}
+
 mp_status check_multi_args(const void* t, const void* x, mp_dtype dt, const int64_t* shape, int order,
                            const mp_norm* levels, int depth, double eta) {
   if (!dtype_ok(dt)) return fail(MP_ERR_CONFIG, "unknown dtype code");
@@ -697,7 +725,11 @@ size_t mp_multilevel_workspace_size(mp_dtype dtype, const int64_t* shape, int or
     return 0;
   Carve c(nullptr, 0);
   carve_multi(c, dtype, shape, order, levels);
-  return c.off + 256;
+  size_t need = c.off + 256;
+  int64_t rows = 0;
+  if (inf_inner_levels(shape, order, levels, rows))
+    need = std::max(need, mp_bilevel_workspace_size(dtype, rows, shape[order - 1], levels[order - 1], MP_NORM_INF));
+  return need;
 }
 
 mp_status mp_multilevel_project(const void* t, void* x, mp_dtype dtype, const int64_t* shape, int order,
@@ -707,6 +739,23 @@ mp_status mp_multilevel_project(const void* t, void* x, mp_dtype dtype, const in
   if (st != MP_OK) return st;
   if (!workspace) return fail(MP_ERR_WORKSPACE, "null workspace");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int64_t rows = 0;
+  if (!budget_chain && inf_inner_levels(shape, order, levels, rows)) {
+    // (inf, ..., inf, p) == bi-level l_{p,inf} on the (d0*...*d_{r-2}, d_{r-1})
+    // reshape, bit for bit: the nested clamps collapse to the
+    // deepest budget because |T| <= every intermediate max.  One norm sweep,
+    // one apply sweep, instead of the level-by-level chain.
+    prof_mark(0, s);
+    if (dtype == MP_F32)
+      st = bilevel_impl<float>(static_cast<const float*>(t), static_cast<float*>(x), dtype, rows, shape[order - 1],
+                               levels[order - 1], MP_NORM_INF, eta, nullptr, nullptr, info, flags, workspace,
+                               workspace_bytes, s);
+    else
+      st = bilevel_impl<double>(static_cast<const double*>(t), static_cast<double*>(x), dtype, rows, shape[order - 1],
+                                levels[order - 1], MP_NORM_INF, eta, nullptr, nullptr, info, flags, workspace,
+                                workspace_bytes, s);
+    return st;
+  }
   if (dtype == MP_F32)
     return multilevel_impl<float>(static_cast<const float*>(t), static_cast<float*>(x), dtype, shape, order, levels,
                                   eta, budget_chain, info, flags, workspace, workspace_bytes, s);

@@ -167,8 +167,10 @@ mp_status mp_multilevel_project_host(mp_context* ctx, const void* t, void* x, mp
   mp_info* d_info = reinterpret_cast<mp_info*>(static_cast<char*>(ctx->small) + small);
   cudaStream_t s = ctx->stream;
   MP_CUDA_TRY(cudaMemcpyAsync(ctx->data, t, bytes, cudaMemcpyHostToDevice, s));
+  // A NULL budget_chain lets the device pick the collapsed (inf, ..., inf, p) path.
   mp_status st = mp_multilevel_project(ctx->data, ctx->data, dtype, shape, order, levels, depth, eta,
-                                       chain_len ? d_chain : nullptr, d_info, flags, ctx->ws, ctx->ws_cap, s);
+                                       (budget_chain && chain_len) ? d_chain : nullptr, d_info, flags, ctx->ws,
+                                       ctx->ws_cap, s);
   if (st != MP_OK) return st;
   mp_info info{};
   MP_CUDA_TRY(cudaMemcpyAsync(&info, d_info, sizeof info, cudaMemcpyDeviceToHost, s));

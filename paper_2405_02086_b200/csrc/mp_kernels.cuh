@@ -157,33 +157,44 @@ __device__ __forceinline__ T* step_ptr(T* p, int64_t elems) {
 // time, i.e. one contiguous ~R*m*sizeof(T) region of HBM).
 // `rpb` doubles as the interleaved quotient: with interleave the host passes
 // rpb = n / R, so slot b owns rpb + (b < n % R) rows (no device division).
+// Row slots are (blockIdx.y, threadIdx.y): R = gridDim.y * blockDim.y.
 struct RowWalk {
   int64_t r0, step, cnt;
 };
+template <bool RG = false>
 __device__ __forceinline__ RowWalk row_walk(int64_t n, int64_t rpb, int interleave) {
-  const int64_t b = blockIdx.y, R = gridDim.y;
+  const int64_t b = RG ? static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y : blockIdx.y;
+  const int64_t R = RG ? static_cast<int64_t>(gridDim.y) * blockDim.y : gridDim.y;
   if (interleave) return {b, R, rpb + (b < n - rpb * R ? 1 : 0)};
   const int64_t r0 = b * rpb;
   return {r0, 1, r0 < n ? min(rpb, n - r0) : 0};
 }
 
-template <typename T, int VEC, int Q, int U>
-__global__ void __launch_bounds__(kThreads)
+// K1.  blockDim = (column threads, row groups): narrow matrices (few column
+// threads) stack up to 16 row groups in one CTA and fold them in shared
+// memory first, so each column sees one atomic / partial per CTA instead of
+// one per row group (atomics on few addresses serialise in L2).
+template <typename T, int VEC, int Q, int U, bool RG>
+__global__ void __launch_bounds__(RG ? 1024 : kThreads, RG ? 1 : 8)
     k_colnorm(const T* __restrict__ y, int64_t n, int64_t m, int64_t rpb, int interleave, void* __restrict__ out) {
   pdl_trigger();  // let the (single-CTA) outer kernel be scheduled as SMs free up
   tl_begin(0);
   const int64_t c0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * VEC;
-  if (c0 >= m) return;
-  const RowWalk rw = row_walk(n, rpb, interleave);
-  const int64_t ds = rw.step * m;  // element stride between consecutive rows of this CTA
-  const T* p = y + rw.r0 * m + c0;
+  if constexpr (!RG) {
+    if (c0 >= m) return;
+  }
+  const bool active = !RG || c0 < m;
+  const RowWalk rw = row_walk<RG>(n, rpb, interleave);
+  const int64_t cnt = RG ? (active ? rw.cnt : 0) : rw.cnt;
+  const int64_t ds = rw.step * m;  // element stride between consecutive rows of this thread
+  const T* p = y + rw.r0 * m + (active ? c0 : 0);
   int64_t k = 0;
   if constexpr (Q == kInf) {
     using B = typename BitsT<T>::type;
     B acc[VEC];
 #pragma unroll
     for (int j = 0; j < VEC; ++j) acc[j] = 0;
-    for (; k + U <= rw.cnt; k += U) {
+    for (; k + U <= cnt; k += U) {
       T e[U][VEC];
 #pragma unroll
       for (int u = 0; u < U; ++u) {  // one live address: p advances load by load
@@ -195,12 +206,25 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int j = 0; j < VEC; ++j) acc[j] = max(acc[j], abs_bits(e[u][j]));
     }
-    for (; k < rw.cnt; ++k, p += ds) {
+    for (; k < cnt; ++k, p += ds) {
       T e[VEC];
       load_keep<T, VEC>(p, e);
 #pragma unroll
       for (int j = 0; j < VEC; ++j) acc[j] = max(acc[j], abs_bits(e[j]));
     }
+    if (RG) {  // fold the row groups (max is order-free)
+      extern __shared__ unsigned char k1_smem[];
+      B* red = reinterpret_cast<B*>(k1_smem);
+      const int slot = (threadIdx.y * blockDim.x + threadIdx.x) * VEC;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) red[slot + j] = acc[j];
+      __syncthreads();
+      if (threadIdx.y != 0) return;
+      for (int r = 1; r < static_cast<int>(blockDim.y); ++r)
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) acc[j] = max(acc[j], red[(r * blockDim.x + threadIdx.x) * VEC + j]);
+    }
+    if (RG && !active) return;
     B* vb = static_cast<B*>(out) + c0;
 #pragma unroll
     for (int j = 0; j < VEC; ++j) atomicMax(vb + j, acc[j]);
@@ -209,7 +233,7 @@ __global__ void __launch_bounds__(kThreads)
     double acc[VEC];
 #pragma unroll
     for (int j = 0; j < VEC; ++j) acc[j] = 0.0;
-    for (; k + U <= rw.cnt; k += U) {
+    for (; k + U <= cnt; k += U) {
       T e[U][VEC];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -224,7 +248,7 @@ __global__ void __launch_bounds__(kThreads)
           acc[j] = (Q == kL1) ? __dadd_rn(acc[j], fabs(dv)) : __dadd_rn(acc[j], __dmul_rn(dv, dv));
         }
     }
-    for (; k < rw.cnt; ++k, p += ds) {
+    for (; k < cnt; ++k, p += ds) {
       T e[VEC];
       load_keep<T, VEC>(p, e);
 #pragma unroll
@@ -233,6 +257,19 @@ __global__ void __launch_bounds__(kThreads)
         acc[j] = (Q == kL1) ? __dadd_rn(acc[j], fabs(dv)) : __dadd_rn(acc[j], __dmul_rn(dv, dv));
       }
     }
+    if (RG) {  // fold the row groups in fixed order (deterministic)
+      extern __shared__ unsigned char k1_smem[];
+      double* red = reinterpret_cast<double*>(k1_smem);
+      const int slot = (threadIdx.y * blockDim.x + threadIdx.x) * VEC;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) red[slot + j] = acc[j];
+      __syncthreads();
+      if (threadIdx.y != 0) return;
+      for (int r = 1; r < static_cast<int>(blockDim.y); ++r)
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) acc[j] = __dadd_rn(acc[j], red[(r * blockDim.x + threadIdx.x) * VEC + j]);
+    }
+    if (RG && !active) return;
     double* part = static_cast<double*>(out) + static_cast<int64_t>(blockIdx.y) * m + c0;
 #pragma unroll
     for (int j = 0; j < VEC; ++j) part[j] = acc[j];

@@ -126,7 +126,7 @@ t = datagen.config_input(4)
 eta = 0.05 * float(np.abs(t).max(axis=0).max(axis=0).astype(np.float64).sum())
 td_ = torch.from_numpy(t).to(dev)
 xd = torch.empty_like(td_)
-mpj = mp.MultilevelProjector(t.shape, "inf,inf,1", device=dev)
+mpj = mp.MultilevelProjector(t.shape, "inf,inf,1", device=dev, want_chain=False)
 ms = timed_graph(lambda: mpj(td_, xd, eta, stream=stream))
 mpj(td_, xd, eta); torch.cuda.synchronize()
 cpu_s = None

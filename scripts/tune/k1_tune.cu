@@ -18,7 +18,7 @@ __global__ void flush_read(const float4* p, size_t n, float* out) {
 template <int VEC, int U, int IL>
 void run(const char* name, const float* y, int64_t n, int64_t m, unsigned* out, int ctas_per_sm, const float4* fl,
          size_t fln, float* fo) {
-  auto fn = mpk::k_colnorm<float, VEC, mpk::kInf, U>;
+  auto fn = mpk::k_colnorm<float, VEC, mpk::kInf, U, false>;
   int64_t slots = m / VEC;
   int64_t tiles = (slots + 255) / 256;
   int threads = (int)((slots + tiles - 1) / tiles);
