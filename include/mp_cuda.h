@@ -150,6 +150,16 @@ mp_status mp_bilevel_project_host(mp_context* ctx, const void* y, void* x, mp_dt
                                   double* budgets, int64_t* zero_columns, double* tau,
                                   unsigned flags);
 
+/* Radius sweep with host buffers (the reference's run_radius_sweep shape,
+ * proj/src/bench.cpp:93-106): y is uploaded once and projected at each of
+ * count radii; xs[k] (host) receives the k-th projection.  Downloads overlap
+ * the next projection (two device output buffers, a copy stream).  budgets
+ * (count * m doubles) and zero_columns (count) are nullable host outputs.
+ * On a device-side failure the xs contents are unspecified. */
+mp_status mp_bilevel_sweep_host(mp_context* ctx, const void* y, void* const* xs, mp_dtype dtype, int64_t n,
+                                int64_t m, mp_norm p, mp_norm q, const double* etas, int count,
+                                double* budgets, int64_t* zero_columns, unsigned flags);
+
 mp_status mp_multilevel_project_host(mp_context* ctx, const void* t, void* x, mp_dtype dtype,
                                      const int64_t* shape, int order, const mp_norm* levels,
                                      int depth, double eta, double* budget_chain,

@@ -24,7 +24,7 @@ from ._capi import (MP_F32, MP_F64, MP_FLAG_EXACT_ZERO_SIGN, MpInfo, MpConfigErr
                     ProjectionError, check, lib, norm_code, parse_norm_spec)
 
 __all__ = [
-    "bilevel_project", "multilevel_project", "trilevel_project_l1infinf", "project_l1", "project_l2",
+    "bilevel_project", "bilevel_radius_sweep", "multilevel_project", "trilevel_project_l1infinf", "project_l1", "project_l2",
     "project_linf", "project_ball", "matrix_pq_norm", "multilevel_norm", "aggregate_leading_axis",
     "structured_sparsity", "gen_uniform_matrix", "perturb_gaussian", "BilevelProjector", "MultilevelProjector",
     "ProjectionError", "MpValueError", "MpShapeError", "MpConfigError", "MP_FLAG_EXACT_ZERO_SIGN",
@@ -171,6 +171,25 @@ def bilevel_project(y, eta, p="1", q="inf", workers=1, flags: int = 0):
     check(lib().mp_bilevel_project_host(None, arr.ctypes.data, x.ctypes.data, _dt(arr), n, m, pc, qc, float(eta),
                                         budgets.ctypes.data, C.addressof(z), C.addressof(tau), flags))
     return x, budgets.tolist(), int(z.value)
+
+
+def bilevel_radius_sweep(y, etas, p="1", q="inf", flags: int = 0):
+    """Project one host matrix at several radii (the reference's radius sweep,
+    proj/src/bench.cpp:93-106): one upload, downloads overlapped with the next
+    projection.  Returns a list of (X, budgets, zero_columns)."""
+    pc, qc = norm_code(p), norm_code(q)
+    arr = _host_array(y)
+    if arr.ndim != 2:
+        raise MpShapeError("bilevel_project requires order 2")
+    n, m = arr.shape
+    etas = np.ascontiguousarray(etas, np.float64)
+    xs = [np.empty_like(arr) for _ in etas]
+    ptrs = (C.c_void_p * len(xs))(*[x.ctypes.data for x in xs])
+    budgets = np.empty((len(etas), m), np.float64)
+    zeros = np.empty(len(etas), np.int64)
+    check(lib().mp_bilevel_sweep_host(None, arr.ctypes.data, ptrs, _dt(arr), n, m, pc, qc, etas.ctypes.data,
+                                      len(etas), budgets.ctypes.data, zeros.ctypes.data, flags))
+    return [(xs[k], budgets[k].tolist(), int(zeros[k])) for k in range(len(etas))]
 
 
 def multilevel_project(y, norms, eta, workers=1, flags: int = 0, return_chain: bool = False):

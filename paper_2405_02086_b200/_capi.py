@@ -22,7 +22,7 @@ EXPORTS = [
     "mp_project_ball_workspace_size", "mp_project_ball",
     "mp_aggregate_workspace_size", "mp_aggregate",
     "mp_context_create", "mp_context_destroy",
-    "mp_bilevel_project_host", "mp_multilevel_project_host",
+    "mp_bilevel_project_host", "mp_bilevel_sweep_host", "mp_multilevel_project_host",
     "mp_project_ball_host", "mp_aggregate_host", "mp_perturb_gaussian",
     "mp_profile_events", "mp_profile_timeline", "mp_last_error", "mp_version",
 ]
@@ -89,6 +89,8 @@ def lib() -> C.CDLL:
     L.mp_context_destroy.restype = None
     L.mp_bilevel_project_host.argtypes = [vp, vp, vp, en, i64, i64, en, en, dbl, vp, vp, vp, u32]
     L.mp_bilevel_project_host.restype = st
+    L.mp_bilevel_sweep_host.argtypes = [vp, vp, vp, en, i64, i64, en, en, vp, C.c_int, vp, vp, u32]
+    L.mp_bilevel_sweep_host.restype = st
     L.mp_multilevel_project_host.argtypes = [vp, vp, vp, en, vp, C.c_int, vp, C.c_int, dbl, vp, u32]
     L.mp_multilevel_project_host.restype = st
     L.mp_project_ball_host.argtypes = [vp, vp, vp, en, i64, en, dbl]

@@ -20,6 +20,10 @@ using namespace mpi;
 struct mp_context {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // D2H of sweep results (overlaps the next projection)
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  void* out2 = nullptr;  // second output buffer for the sweep ping-pong
+  size_t out2_cap = 0;
   std::mutex mu;
   void* data = nullptr;  // tensor buffer (projected in place)
   size_t data_cap = 0;
@@ -76,11 +80,13 @@ mp_context* mp_context_create(int device) {
   auto* c = new mp_context();
   c->device = device;
   DeviceGuard g(device);
-  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
-    set_error("mp_context_create: cannot create a stream on device %d", device);
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    set_error("mp_context_create: cannot create streams on device %d", device);
     delete c;
     return nullptr;
   }
+  for (auto& e : c->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   return c;
 }
 
@@ -92,6 +98,11 @@ void mp_context_destroy(mp_context* c) {
     if (c->data) cudaFree(c->data);
     if (c->ws) cudaFree(c->ws);
     if (c->small) cudaFree(c->small);
+    if (c->out2) cudaFree(c->out2);
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+    for (auto& e : c->ev)
+      if (e) cudaEventDestroy(e);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->stream) cudaStreamDestroy(c->stream);
   }
   delete c;
@@ -133,6 +144,68 @@ mp_status mp_bilevel_project_host(mp_context* ctx, const void* y, void* x, mp_dt
   MP_CUDA_TRY(cudaStreamSynchronize(s));
   if (zero_columns) *zero_columns = info.zero_columns;
   if (tau) *tau = info.tau;
+  return MP_OK;
+}
+
+mp_status mp_bilevel_sweep_host(mp_context* ctx, const void* y, void* const* xs, mp_dtype dtype, int64_t n, int64_t m,
+                                mp_norm p, mp_norm q, const double* etas, int count, double* budgets,
+                                int64_t* zero_columns, unsigned flags) {
+  if (!ctx) ctx = default_ctx();
+  if (!ctx) return fail(MP_ERR_CUDA, "no CUDA context");
+  if (count < 0 || (count > 0 && (!etas || !xs))) return fail(MP_ERR_CONFIG, "bad sweep arguments");
+  if (count == 0) return MP_OK;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g(ctx->device);
+  const size_t ws = mp_bilevel_workspace_size(dtype, n, m, p, q);
+  if (ws == 0)
+    return mp_bilevel_project(y, xs[0], dtype, n, m, p, q, etas[0], nullptr, nullptr, nullptr, flags, nullptr, 0,
+                              nullptr);
+  for (int k = 0; k < count; ++k)
+    if (!(etas[k] >= 0.0) || !std::isfinite(etas[k]))
+      return fail(MP_ERR_VALUE, "radius must be a finite nonnegative real");
+  if (!y) return fail(MP_ERR_WORKSPACE, "null tensor pointer");
+  const size_t bytes = static_cast<size_t>(n) * static_cast<size_t>(m) * dtype_size(dtype);
+  const size_t per = ((static_cast<size_t>(m) * sizeof(double) + sizeof(mp_info) + 255) / 256) * 256;
+  MP_CUDA_TRY(grow(ctx->data, ctx->data_cap, 2 * ((bytes + 255) / 256) * 256));  // y + out[0]
+  MP_CUDA_TRY(grow(ctx->out2, ctx->out2_cap, bytes));                           // out[1]
+  MP_CUDA_TRY(grow(ctx->ws, ctx->ws_cap, ws));
+  MP_CUDA_TRY(grow(ctx->small, ctx->small_cap, per * static_cast<size_t>(count)));
+  char* dy = static_cast<char*>(ctx->data);
+  void* dout[2] = {dy + ((bytes + 255) / 256) * 256, ctx->out2};
+  cudaStream_t s = ctx->stream, cs = ctx->copy_stream;
+  // One upload; each projection writes a ping-pong buffer whose download on
+  // the copy stream overlaps the next projection (the reference's radius
+  // sweep, proj/src/bench.cpp:93-106, re-uploads nothing either).
+  MP_CUDA_TRY(cudaMemcpyAsync(dy, y, bytes, cudaMemcpyHostToDevice, s));
+  for (int k = 0; k < count; ++k) {
+    const int b = k & 1;
+    char* sm = static_cast<char*>(ctx->small) + per * k;
+    if (k >= 2) MP_CUDA_TRY(cudaStreamWaitEvent(s, ctx->ev[2 + b], 0));  // buffer b downloaded
+    mp_status st = mp_bilevel_project(dy, dout[b], dtype, n, m, p, q, etas[k], reinterpret_cast<double*>(sm), nullptr,
+                                      reinterpret_cast<mp_info*>(sm + static_cast<size_t>(m) * sizeof(double)), flags,
+                                      ctx->ws, ctx->ws_cap, s);
+    if (st != MP_OK) return st;
+    MP_CUDA_TRY(cudaEventRecord(ctx->ev[b], s));
+    MP_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[b], 0));
+    MP_CUDA_TRY(cudaMemcpyAsync(xs[k], dout[b], bytes, cudaMemcpyDeviceToHost, cs));
+    MP_CUDA_TRY(cudaEventRecord(ctx->ev[2 + b], cs));
+  }
+  std::vector<mp_info> infos(static_cast<size_t>(count));
+  for (int k = 0; k < count; ++k) {
+    char* sm = static_cast<char*>(ctx->small) + per * k;
+    MP_CUDA_TRY(cudaMemcpyAsync(&infos[k], sm + static_cast<size_t>(m) * sizeof(double), sizeof(mp_info),
+                                cudaMemcpyDeviceToHost, s));
+    if (budgets)
+      MP_CUDA_TRY(cudaMemcpyAsync(budgets + static_cast<size_t>(k) * m, sm, static_cast<size_t>(m) * sizeof(double),
+                                  cudaMemcpyDeviceToHost, s));
+  }
+  MP_CUDA_TRY(cudaStreamSynchronize(s));
+  MP_CUDA_TRY(cudaStreamSynchronize(cs));
+  for (int k = 0; k < count; ++k) {
+    mp_status st = device_status(infos[k]);
+    if (st != MP_OK) return st;
+    if (zero_columns) zero_columns[k] = infos[k].zero_columns;
+  }
   return MP_OK;
 }
 

@@ -336,3 +336,14 @@ def test_perturbation_is_seeded_gaussian():
     assert not torch.equal(a, c)
     m, s = float(a.mean()), float(a.std())
     assert abs(m) < 5e-3 and abs(s - 1.0) < 5e-3
+
+
+def test_radius_sweep_host_api_matches_single_calls():
+    y = datagen.uniform(21, (3000, 2000), -1.0, 1.0)
+    colsum = float(np.abs(y).max(axis=0).astype(np.float64).sum())
+    etas = [0.001 * colsum, 0.1 * colsum, 0.5 * colsum, 2.0 * colsum, 0.0]
+    res = mp.bilevel_radius_sweep(y, etas)
+    for (x, b, z), e in zip(res, etas):
+        x1, b1, z1 = mp.bilevel_project(y, e)
+        assert bit_equal(x, x1) and z == z1
+        np.testing.assert_array_equal(np.asarray(b), np.asarray(b1))
