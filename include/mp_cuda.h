@@ -133,6 +133,18 @@ mp_status mp_aggregate(const void* t, double* out, mp_dtype dtype, int64_t n, in
 mp_status mp_perturb_gaussian(void* x, mp_dtype dtype, int64_t count, double sigma, uint64_t seed,
                               uint64_t iteration, void* stream);
 
+size_t mp_project_fibers_workspace_size(mp_dtype dtype, int64_t n, int64_t m, mp_norm q);
+
+/* The apply seam alone (detail::project_block,
+ * proj/include/multiproj/detail/fiber_kernels.hpp:16-20,
+ * proj/src/fiber_kernels.cpp:37-67): every fiber (column) j of the (n, m)
+ * view is projected onto the q-ball of radius budgets[j], given its q-norm
+ * norms[j] (both device, f64).  Used by the column-sharded multi-GPU
+ * projection, where the budgets come from a gathered norm vector. */
+mp_status mp_project_fibers(const void* y, void* x, mp_dtype dtype, int64_t n, int64_t m, mp_norm q,
+                            const double* norms, const double* budgets, unsigned flags, void* workspace,
+                            size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------------ host */
 
 /* Opaque per-thread-safe execution context: device, stream, cached device

@@ -255,6 +255,10 @@ static void project_fibers(double* x, int64_t n, int64_t m, int q,
   }
 }
 
+void orc_project_fibers(double* x, int64_t n, int64_t m, int q, const double* v, const double* budgets) {
+  project_fibers(x, n, m, q, v, budgets);
+}
+
 int orc_bilevel(const double* y, int64_t n, int64_t m, int p, int q,
                 double eta, double* x, double* budgets, double* v,
                 int64_t* zero_columns, double* tau) {

@@ -46,6 +46,9 @@ void orc_project_l1_sort_inplace(double* y, int64_t len, double radius,
  * finiteness, then projects y in place onto the q-ball. */
 int orc_project_ball(double* y, int64_t len, int q, double radius);
 
+/* detail::project_block over all fibers, in place (proj/src/fiber_kernels.cpp:37-67). */
+void orc_project_fibers(double* x, int64_t n, int64_t m, int q, const double* v, const double* budgets);
+
 /* bilevel_project (proj/src/bilevel.cpp:10-32).  x, budgets, v (norms) and
  * zero_columns are outputs; v/tau may be NULL.  tau is the outer l1
  * threshold (-1 when the outer step was the identity / p != 1). */

@@ -82,6 +82,8 @@ def lib():
         L.orc_multilevel_norm.restype = C.c_int
         L.orc_vector_norm.argtypes = [_P_D, C.c_int64, C.c_int, C.POINTER(C.c_double)]
         L.orc_vector_norm.restype = C.c_int
+        L.orc_project_fibers.argtypes = [_P_D, C.c_int64, C.c_int64, C.c_int, _P_D, _P_D]
+        L.orc_project_fibers.restype = None
         L.orc_structured_sparsity.argtypes = [_P_D, C.c_int64, C.c_int64, C.c_double]
         L.orc_structured_sparsity.restype = C.c_int64
         _lib = L
@@ -210,6 +212,13 @@ def multilevel_norm(t, levels) -> float:
 
 def matrix_pq_norm(y, p, q) -> float:
     return multilevel_norm(y, [q, p])
+
+
+def project_fibers(y, q, v, budgets):
+    """Columns of y projected onto q-balls of radii budgets given norms v."""
+    x = _d(y).copy()
+    lib().orc_project_fibers(x.reshape(-1), x.shape[0], x.size // x.shape[0], _norm(q), _d(v), _d(budgets))
+    return x
 
 
 def structured_sparsity(x, tol=0.0) -> int:

@@ -809,6 +809,42 @@ mp_status mp_project_ball(const void* y, void* x, mp_dtype dtype, int64_t len, m
   return vector_impl(y, x, dtype, len, q, radius, info, w, static_cast<cudaStream_t>(stream));
 }
 
+size_t mp_project_fibers_workspace_size(mp_dtype dtype, int64_t n, int64_t m, mp_norm q) {
+  if (n < 1 || m < 1 || !dtype_ok(dtype) || !norm_ok(q)) return 0;
+  Carve c(nullptr, 0);
+  c.take<mp_info>(1);
+  c.take<double>(m);
+  mpk::carve_l1strip(c, m);
+  return c.off + 256;
+}
+
+mp_status mp_project_fibers(const void* y, void* x, mp_dtype dtype, int64_t n, int64_t m, mp_norm q,
+                            const double* norms, const double* budgets, unsigned flags, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  if (!dtype_ok(dtype)) return fail(MP_ERR_CONFIG, "unknown dtype code");
+  if (!norm_ok(q)) return fail(MP_ERR_CONFIG, "unknown norm code");
+  if (n < 1 || m < 1) return fail(MP_ERR_SHAPE, "project_fibers requires a non-empty (n, m) view");
+  if (!y || !x || !norms || !budgets || !workspace) return fail(MP_ERR_WORKSPACE, "null pointer");
+  Carve c(workspace, workspace_bytes);
+  mp_info* inf = c.take<mp_info>(1);
+  void* colp = c.take<double>(m);
+  mpk::L1StripWs l1 = mpk::carve_l1strip(c, m);
+  if (!c.fits()) return fail(MP_ERR_WORKSPACE, "mp_project_fibers: workspace too small");
+  MP_CUDA_TRY(outer_setup());
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  MP_CUDA_TRY(cudaMemsetAsync(inf, 0, sizeof(mp_info), s));  // status MP_OK: the kernels proceed
+  if (dtype == MP_F32) {
+    MP_CUDA_TRY(launch_colparams<float>(norms, budgets, m, q, colp, inf, s));
+    MP_CUDA_TRY(project_fibers<float>(static_cast<const float*>(y), static_cast<float*>(x), n, m, q, norms, budgets,
+                                      colp, l1, inf, flags, dtype, s));
+  } else {
+    MP_CUDA_TRY(launch_colparams<double>(norms, budgets, m, q, colp, inf, s));
+    MP_CUDA_TRY(project_fibers<double>(static_cast<const double*>(y), static_cast<double*>(x), n, m, q, norms,
+                                       budgets, colp, l1, inf, flags, dtype, s));
+  }
+  return MP_OK;
+}
+
 size_t mp_aggregate_workspace_size(mp_dtype dtype, int64_t n, int64_t m, mp_norm q) {
   if (n < 1 || m < 1 || !dtype_ok(dtype) || !norm_ok(q)) return 0;
   return aggregate_scratch_bytes(dtype, n, m, q) + 256;
