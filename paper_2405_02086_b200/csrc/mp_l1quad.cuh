@@ -88,37 +88,32 @@ __global__ void __launch_bounds__(kQuadThreads)
     double S = 0.0;
     bool done = kind != 3;
     if (done) cnt = 0;
+    long long ckp1 = 0;
     for (int pass = 0; pass < 4 * 1024; ++pass) {
+      if (pass == 1) ckp1 = clock64();
       ++npass;
       const T thr = round_down_to(T(0), t);
       // Batches of 8: all loads first (independent LDS in flight), then the
       // compacting stores -- they land at slots <= the batch's own, so the
       // batch is read before it can be overwritten.
-      constexpr int64_t kStep = static_cast<int64_t>(LPC) * C4;
+      constexpr int kStep = LPC * C4;  // slot stride of one thread (elements)
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int kept = 0, j = 0;
-      for (; j + 8 <= cnt; j += 8) {
+      int kept = 0;
+      for (int j = 0; j < cnt; j += 8) {  // masked batches: no serial tail loop
         T a[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) a[q] = fabs(mine[kStep * (j + q)]);
+        for (int q = 0; q < 8; ++q) a[q] = (j + q < cnt) ? fabs(mine[kStep * (j + q)]) : T(0);
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const bool kq = a[q] > thr;
+          const bool kq = a[q] > thr;  // masked entries are 0 <= thr
           const double dq = kq ? static_cast<double>(a[q]) : 0.0;
           if ((q & 3) == 0) s0 += dq;
           else if ((q & 3) == 1) s1 += dq;
           else if ((q & 3) == 2) s2 += dq;
           else s3 += dq;
-          mine[kStep * kept] = a[q];  // unconditional: the slot is re-written or dropped
+          if (j + q < cnt) mine[kStep * kept] = a[q];  // the slot is re-written or dropped
           kept += kq;
         }
-      }
-      for (; j < cnt; ++j) {
-        const T a0 = fabs(mine[kStep * j]);
-        const bool k0 = a0 > thr;
-        s0 += k0 ? static_cast<double>(a0) : 0.0;
-        mine[kStep * kept] = a0;
-        kept += k0;
       }
       s0 += s2;
       s1 += s3;
@@ -159,6 +154,7 @@ __global__ void __launch_bounds__(kQuadThreads)
       }
       if (!__syncthreads_or(!done)) break;
     }
+    if (threadIdx.x == 0 && g_mp_timeline && ckp1) atomicAdd(g_mp_timeline + 14, static_cast<unsigned long long>(ckp1 - ck1));
     if (kind == 3 && g == 0 && k == 0) stau[c] = (S - uj) / static_cast<double>(K);
     __syncthreads();
   }

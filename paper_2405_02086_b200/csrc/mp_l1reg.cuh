@@ -1,0 +1,365 @@
+// mp_l1reg.cuh -- K3b register-resident path: per-column l1-ball projection
+// (the l_{1,1} apply pass, proj/src/fiber_kernels.cpp:56-65 ->
+// project_l1_fast_inplace, proj/src/vector_balls.cpp:150-161) with the
+// strip held ENTIRELY IN REGISTERS.
+//
+// One 512-thread CTA owns a strip of W = 4P f32 (2P f64) adjacent columns
+// over all n <= 8192/P rows; thread t holds 16-byte piece t % P of rows
+// t / P + (512/P) i, i < 16 (64 registers of data, the whole register file
+// of the SM for P = 2, n = 4096).  A warp instruction then touches 32/P rows
+// of 16P bytes (P = 2: whole 32-byte sectors) instead of 32 lines for 16
+// bytes each -- the L1 line rate, not HBM, bounds a 16-byte-per-row walk.
+//  * y is read from HBM exactly once, all loads of a thread in flight,
+//    issued BEFORE griddepcontrol.wait (no earlier kernel of the projection
+//    writes y), overlapping K2;
+//  * Michelot's fixed point (t <- (S(t) - u_j) / K(t), S, K over |y| > t)
+//    runs over registers with full ILP; per pass a warp reduce-scatter and
+//    one CTA barrier; the column lanes of every warp total the warp partials
+//    in warp order (deterministic, identical in every warp);
+//  * the apply shrinks the registers and stores the row pieces: no re-read.
+// (A grid-stride variant prefetching the next strip into shared memory with
+// cp.async measured slower: 283 vs 256 us on config 3.)
+//
+// Passes come in two kinds.  FAST (f32 strips, far from convergence): f32
+// per-thread sums (an f32->f64 convert per element would cost more than the
+// pass), f64 across threads, and a step to a rigorous LOWER bound of the
+// exact iterate: a thread partial sums <= RPT nonnegative f32 terms, so
+// S >= S_exact (1 - RPT 2^-24) and S_lo = S (1 - 2^-17), rounded down, is
+// below S_exact; t' = RD((S_lo - RU(u_j)) / K) <= (S_exact - u_j) / K.
+// Michelot from below stays below tau and the set only shrinks.  EXACT
+// (near convergence -- the count dropped by < 1/16 -- and always for f64
+// strips): f64 sums, plus min |y| over the set.  With t_ex = (S - u_j) / K,
+// the set is the fixed point {|y| > tau} iff min_set |y| > t_ex, and then
+// tau_j = t_ex: the same fixed point (hence the reference's set
+// {|y| >= cutoff}) that the exact iteration reaches -- one pass before it
+// would see its count repeat.  Otherwise the exact step continues from t_ex.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "mp_cuda.h"
+#include "mp_kernels.cuh"
+#include "mp_l1cols.cuh"
+
+namespace mpk {
+
+constexpr int kRegRPT = 16;       // 16-byte row pieces per thread
+constexpr int kRegThreads = 512;  // one CTA per SM (the register file)
+
+template <typename T>
+struct alignas(16) RegPart {
+  double s;
+  int k;
+  T mn;
+};
+
+template <typename T>
+__device__ __forceinline__ RegPart<T> rp_add(const RegPart<T>& a, const RegPart<T>& b) {
+  return {a.s + b.s, a.k + b.k, a.mn < b.mn ? a.mn : b.mn};
+}
+
+template <typename T>
+__device__ __forceinline__ RegPart<T> rp_shfl(const RegPart<T>& a, int o) {
+  return {__shfl_xor_sync(0xffffffffu, a.s, o), __shfl_xor_sync(0xffffffffu, a.k, o),
+          __shfl_xor_sync(0xffffffffu, a.mn, o)};
+}
+
+// Warp reduce-scatter of the C4 per-column partials of every 16-byte piece
+// over the lanes sharing the piece (lane % P): xor 16, 8 split the columns,
+// xor 4 .. P finish.  Afterwards lane l holds the warp total of strip column
+// reg_col<T, P>(l) iff reg_writer<T, P>(l).  Fixed pattern => deterministic.
+template <typename T, int P>
+__device__ __forceinline__ int reg_col(int lane) {
+  constexpr int C4 = 16 / sizeof(T);
+  const int c = C4 == 4 ? ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1) : ((lane >> 4) & 1);
+  return (lane & (P - 1)) * C4 + c;
+}
+template <typename T, int P>
+__device__ __forceinline__ bool reg_writer(int lane) {
+  constexpr int C4 = 16 / sizeof(T);
+  constexpr int hi = C4 == 4 ? 7 : 15;  // bits still reduced after the split
+  return (lane & (hi & ~(P - 1))) == 0;
+}
+
+// Fast-pass partial: f32 sum and count (exact: counts < 2^24).
+struct FastPart {
+  float s, k;
+};
+__device__ __forceinline__ FastPart rp_add(const FastPart& a, const FastPart& b) { return {a.s + b.s, a.k + b.k}; }
+__device__ __forceinline__ FastPart rp_shfl(const FastPart& a, int o) {
+  return {__shfl_xor_sync(0xffffffffu, a.s, o), __shfl_xor_sync(0xffffffffu, a.k, o)};
+}
+
+// Field-wise select (a ternary on the aggregates would index the array with a
+// runtime value and send it to local memory).
+__device__ __forceinline__ FastPart rp_sel(bool p, const FastPart& a, const FastPart& b) {
+  return {p ? a.s : b.s, p ? a.k : b.k};
+}
+template <typename T>
+__device__ __forceinline__ RegPart<T> rp_sel(bool p, const RegPart<T>& a, const RegPart<T>& b) {
+  return {p ? a.s : b.s, p ? a.k : b.k, p ? a.mn : b.mn};
+}
+
+template <int C4, int P, typename Part>
+__device__ __forceinline__ Part reg_reduce(const Part (&a)[C4], int lane) {
+  Part r;
+  if constexpr (C4 == 4) {
+    const bool h4 = lane & 16, h3 = lane & 8;
+    const Part b0 = rp_add(rp_sel(h4, a[2], a[0]), rp_shfl(rp_sel(h4, a[0], a[2]), 16));
+    const Part b1 = rp_add(rp_sel(h4, a[3], a[1]), rp_shfl(rp_sel(h4, a[1], a[3]), 16));
+    r = rp_add(rp_sel(h3, b1, b0), rp_shfl(rp_sel(h3, b0, b1), 8));
+#pragma unroll
+    for (int o = 4; o >= P; o >>= 1) r = rp_add(r, rp_shfl(r, o));
+  } else {
+    const bool h4 = lane & 16;
+    r = rp_add(rp_sel(h4, a[1], a[0]), rp_shfl(rp_sel(h4, a[0], a[1]), 16));
+#pragma unroll
+    for (int o = 8; o >= P; o >>= 1) r = rp_add(r, rp_shfl(r, o));
+  }
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ void reg_unpack(const uint4& q, T (&e)[16 / sizeof(T)]) {
+  if constexpr (sizeof(T) == 4) {
+    e[0] = __uint_as_float(q.x); e[1 % (16 / sizeof(T))] = __uint_as_float(q.y);
+    e[2 % (16 / sizeof(T))] = __uint_as_float(q.z); e[3 % (16 / sizeof(T))] = __uint_as_float(q.w);
+  } else {
+    e[0] = __hiloint2double(static_cast<int>(q.y), static_cast<int>(q.x));
+    e[1 % (16 / sizeof(T))] = __hiloint2double(static_cast<int>(q.w), static_cast<int>(q.z));
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ uint4 reg_pack(const T (&e)[16 / sizeof(T)]) {
+  if constexpr (sizeof(T) == 4) {
+    return make_uint4(__float_as_uint(e[0]), __float_as_uint(e[1 % 4]), __float_as_uint(e[2 % 4]),
+                      __float_as_uint(e[3 % 4]));
+  } else {
+    const double a = e[0], b = e[1 % 2];
+    return make_uint4(static_cast<unsigned>(__double2loint(a)), static_cast<unsigned>(__double2hiint(a)),
+                      static_cast<unsigned>(__double2loint(b)), static_cast<unsigned>(__double2hiint(b)));
+  }
+}
+
+template <typename T, int P, bool DERIVE>
+__global__ void __launch_bounds__(kRegThreads, 1)
+    k_l1reg(const T* __restrict__ y, T* __restrict__ x, int n, int64_t m, const double* __restrict__ v,
+            const double* __restrict__ u, double* __restrict__ tau_out, const mp_info* __restrict__ info,
+            const OuterParams* __restrict__ params, double* __restrict__ u_out) {
+  constexpr int C4 = 16 / sizeof(T);
+  constexpr int W = C4 * P;  // strip columns
+  constexpr int NT = kRegThreads;
+  constexpr int NW = NT / 32;
+  constexpr int SL = NT / P;  // row slots
+  constexpr int RPT = kRegRPT;
+  constexpr bool kF32 = sizeof(T) == 4;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t strip = blockIdx.x;
+  const int pc = (tid % P) * C4;  // this thread's first strip column
+  const int rb = tid / P;         // this thread's first row
+  const int64_t step = static_cast<int64_t>(SL) * m;
+
+  // Land the first strip: y is not written by K1 / K2.
+  uint4 q[RPT];
+  {
+    const T* yp = y + static_cast<int64_t>(rb) * m + strip * W + pc;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i, yp += step)
+      q[i] = rb + SL * i < n ? __ldg(reinterpret_cast<const uint4*>(yp)) : make_uint4(0, 0, 0, 0);
+  }
+  pdl_wait();
+  tl_begin(3);
+  if (info->status != MP_OK) return;
+
+  __shared__ FastPart wf[2][NW][W];
+  __shared__ RegPart<T> wx[2][NW][W];
+  int npass = 0;
+  {
+    const int64_t cb = strip * W + pc;
+    // this thread's columns: kinds (2 bits each: 1 feasible, 2 zero budget,
+    // 3 project), live bits, thresholds
+    unsigned kinds = 0, livem = 0;
+    T thr[C4];
+#pragma unroll
+    for (int c = 0; c < C4; ++c) {
+      const double vj = v[cb + c];
+      const double uj = DERIVE ? derive_u(*params, vj) : u[cb + c];
+      const unsigned kd = vj <= uj ? 1u : (uj == 0.0 ? 2u : 3u);
+      kinds |= kd << (2 * c);
+      livem |= (kd == 3u ? 1u : 0u) << c;
+      // first iterate from the norm pass, nudged below the rounding of v_j
+      thr[c] = round_down_to(T(0), (vj * (1.0 - 0x1p-40) - uj) / static_cast<double>(n));
+    }
+    // strip column `lane` (< W): iteration state, identical in every warp
+    double ul = 0.0, td = -1.0;
+    float uup = 0.0f;  // RU(u_j)
+    int kp = n + 1;
+    bool lv = false, ex = !kF32, pj = false;
+    if (lane < W) {
+      const double vj = v[strip * W + lane];
+      ul = DERIVE ? derive_u(*params, vj) : u[strip * W + lane];
+      uup = __double2float_ru(ul);
+      pj = lv = !(vj <= ul) && ul != 0.0;
+      if (pj) td = (vj * (1.0 - 0x1p-40) - ul) / static_cast<double>(n);
+      if (DERIVE && u_out && warp == 0) u_out[strip * W + lane] = ul;
+    }
+    const bool any_proj = __any_sync(0xffffffffu, pj);
+
+    if (any_proj) {
+      bool xp = !kF32;  // exact pass (CTA-uniform)
+      for (int par = 0, it = 0; it < 4 * 1024; par ^= 1, ++it) {
+        ++npass;
+        if (!xp) {
+          FastPart a[C4];
+#pragma unroll
+          for (int c = 0; c < C4; ++c) {
+            float sf = 0.0f, kf = 0.0f;
+            const float th = (livem >> c) & 1u ? static_cast<float>(thr[c]) : INFINITY;
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+              T e[C4];
+              reg_unpack<T>(q[i], e);
+              const float ab = fabsf(static_cast<float>(e[c]));
+              if (ab > th) {
+                sf += ab;
+                kf += 1.0f;
+              }
+            }
+            a[c] = {sf, kf};
+          }
+          const FastPart wr = reg_reduce<C4, P>(a, lane);
+          if (reg_writer<T, P>(lane)) wf[par][warp][reg_col<T, P>(lane)] = wr;
+        } else {
+          RegPart<T> a[C4];
+#pragma unroll
+          for (int c = 0; c < C4; ++c) {
+            double sd = 0.0;
+            int kk = 0;
+            T mn = T(INFINITY);
+            const T th = (livem >> c) & 1u ? thr[c] : T(INFINITY);
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+              T e[C4];
+              reg_unpack<T>(q[i], e);
+              const T ab = kF32 ? fabsf(e[c]) : fabs(e[c]);
+              if (ab > th) {
+                sd += static_cast<double>(ab);
+                ++kk;
+                mn = ab < mn ? ab : mn;
+              }
+            }
+            a[c] = {sd, kk, mn};
+          }
+          const RegPart<T> wr = reg_reduce<C4, P>(a, lane);
+          if (reg_writer<T, P>(lane)) wx[par][warp][reg_col<T, P>(lane)] = wr;
+        }
+        __syncthreads();
+        if (lane < W && lv) {
+          // column totals over the warps, in warp order
+          RegPart<T> tot;
+          if (xp) {
+            tot = wx[par][0][lane];
+#pragma unroll
+            for (int w = 1; w < NW; ++w) tot = rp_add(tot, wx[par][w][lane]);
+          } else {
+            float s32 = 0.0f, k32 = 0.0f;  // <= RPT + 5 + NW f32 terms per sum
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+              const FastPart f = wf[par][w][lane];
+              s32 += f.s;
+              k32 += f.k;
+            }
+            tot = {static_cast<double>(s32), static_cast<int>(k32), T(INFINITY)};
+          }
+          if (tot.k == 0) {
+            lv = false;  // cannot happen for 0 < u_j < v_j; keep the threshold
+          } else if (xp) {
+            const double tex = (tot.s - ul) / static_cast<double>(tot.k);
+            if (tot.mn > round_down_to(T(0), tex)) {
+              td = tex;  // the fixed point: tau_j
+              lv = false;
+            } else {
+              td = fmax(td, tex);
+              kp = tot.k;
+            }
+          } else {
+            // a rigorous lower bound of (S_exact - u_j) / K: the f32 sums
+            // carry < 40 * 2^-24 relative error, the margin is 2^-17
+            const float xs = __fsub_rd(__fmul_rd(__double2float_rd(tot.s), 1.0f - 0x1p-17f), uup);
+            const float tn = xs > 0.0f ? __fmul_rd(xs, __frcp_rd(static_cast<float>(tot.k))) : 0.0f;
+            td = fmax(td, static_cast<double>(tn));
+            if ((kp - tot.k) * 16 <= tot.k) ex = true;  // near convergence: exact steps from here
+            kp = tot.k;
+          }
+        }
+        const T tl = round_down_to(T(0), td);
+#pragma unroll
+        for (int c = 0; c < C4; ++c) thr[c] = __shfl_sync(0xffffffffu, tl, pc + c);
+        const unsigned lvb = __ballot_sync(0xffffffffu, lv);
+        livem = (lvb >> pc) & ((1u << C4) - 1u);
+        if (lvb == 0u) break;
+        xp = xp || __ballot_sync(0xffffffffu, lv && ex) != 0u;
+      }
+    }
+    if (warp == 0 && lane < W) tau_out[strip * W + lane] = pj ? td : -1.0;
+
+    // ---- apply from registers
+    bool need_store = any_proj || x != y;
+#pragma unroll
+    for (int c = 0; c < C4; ++c) need_store = need_store || ((kinds >> (2 * c)) & 3u) == 2u;
+    need_store = __syncthreads_or(need_store);
+    if (need_store) {
+      double t[C4];
+      TauPair tp[C4];
+#pragma unroll
+      for (int c = 0; c < C4; ++c) {
+        t[c] = __shfl_sync(0xffffffffu, td, pc + c);
+        tp[c].hi = __double2float_rn(t[c]);
+        tp[c].lo = __double2float_rn(t[c] - static_cast<double>(tp[c].hi));
+      }
+      T* xq = x + static_cast<int64_t>(rb) * m + cb;
+#pragma unroll
+      for (int i = 0; i < RPT; ++i, xq += step) {
+        if (rb + SL * i >= n) break;
+        T e[C4];
+        reg_unpack<T>(q[i], e);
+#pragma unroll
+        for (int c = 0; c < C4; ++c) {
+          const unsigned kd = (kinds >> (2 * c)) & 3u;
+          if (kd == 2u) e[c] = T(0);
+          else if (kd == 3u) {
+            if constexpr (kF32) {
+              const float dm = shrink_mag(fabsf(e[c]), tp[c]);
+              e[c] = dm > 0.0f ? copysignf(dm, e[c]) : 0.0f;
+            } else {
+              const double dm = fabs(e[c]) - t[c];
+              e[c] = dm > 0.0 ? copysign(dm, e[c]) : 0.0;
+            }
+          }
+        }
+        __stcs(reinterpret_cast<uint4*>(xq), reg_pack<T>(e));
+      }
+    }
+  }
+  if (tid == 0 && g_mp_timeline) {  // profiling aid: passes, slots 8..10
+    atomicAdd(g_mp_timeline + 8, static_cast<unsigned long long>(npass));
+    atomicMax(g_mp_timeline + 9, static_cast<unsigned long long>(npass));
+    atomicAdd(g_mp_timeline + 10, 1ull);
+  }
+  tl_end(3);
+}
+
+// Pieces per row for the register path: the widest P whose 8192/P rows hold
+// the column and that divides the columns; 0 when the path does not apply.
+template <typename T>
+inline int l1reg_pieces(int64_t n, int64_t m, int cap) {
+  constexpr int C4 = 16 / sizeof(T);
+  for (int P = 8; P >= 1; P >>= 1) {
+    if (cap > 0 && P > cap) continue;
+    if (n <= static_cast<int64_t>(kRegThreads / P) * kRegRPT && m % (C4 * P) == 0) return P;
+  }
+  return 0;
+}
+
+}  // namespace mpk

@@ -21,7 +21,10 @@
 // global memory (L2), C = 1.
 #pragma once
 
+#include <algorithm>
 #include <cooperative_groups.h>
+#include <cstdlib>
+#include <cstring>
 #include <cuda_runtime.h>
 
 #include "mp_cuda.h"
@@ -29,6 +32,7 @@
 #include "mp_kernels.cuh"
 #include "mp_l1cols.cuh"
 #include "mp_l1quad.cuh"
+#include "mp_l1reg.cuh"
 
 namespace mpk {
 
@@ -274,6 +278,44 @@ struct L1Derive {
   mp_info* info_w = nullptr;
 };
 
+// MP_L1_KERNEL=quad forces the shared-memory path (A/B timing aid).
+inline bool l1reg_disabled() {
+  static const bool d = [] {
+    const char* e = std::getenv("MP_L1_KERNEL");
+    return e && std::strcmp(e, "quad") == 0;
+  }();
+  return d;
+}
+
+// MP_L1REG_P=1|2|4|8 caps the register path's pieces per row (tuning aid).
+inline int l1reg_prefer_p() {
+  static const int p = [] {
+    const char* e = std::getenv("MP_L1REG_P");
+    return e ? std::atoi(e) : 0;
+  }();
+  return p;
+}
+
+template <typename T, int P>
+cudaError_t launch_reg(const T* y, T* x, int64_t n, int64_t m, const double* v, const double* u,
+                       const L1StripWs& ws, const mp_info* info, const L1Derive& dv, cudaStream_t s) {
+  constexpr int W = 16 / sizeof(T) * P;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kRegThreads);
+  cfg.gridDim = dim3(static_cast<unsigned>(m / W));
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (dv.params)
+    return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, true>, y, x, static_cast<int>(n), m, v, u, ws.tau, info, dv.params,
+                              dv.u_out);
+  return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, false>, y, x, static_cast<int>(n), m, v, u, ws.tau, info, dv.params,
+                            dv.u_out);
+}
+
 template <typename T>
 cudaError_t quad_attr() {
   cudaError_t e = cudaFuncSetAttribute(k_l1quad<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -327,6 +369,15 @@ template <typename T>
 cudaError_t launch_l1strip(const T* y, T* x, int64_t n, int64_t m, const double* v, const double* u,
                            const L1StripWs& ws, const mp_info* info, unsigned flags, cudaStream_t s,
                            const L1Derive& dv = L1Derive()) {
+  if (l1_quad_ok<T>(y, x, m) && !l1reg_disabled()) {
+    switch (l1reg_pieces<T>(n, m, l1reg_prefer_p())) {
+      case 8: return launch_reg<T, 8>(y, x, n, m, v, u, ws, info, dv, s);
+      case 4: return launch_reg<T, 4>(y, x, n, m, v, u, ws, info, dv, s);
+      case 2: return launch_reg<T, 2>(y, x, n, m, v, u, ws, info, dv, s);
+      case 1: return launch_reg<T, 1>(y, x, n, m, v, u, ws, info, dv, s);
+      default: break;
+    }
+  }
   if (l1_quad_ok<T>(y, x, m) && static_cast<size_t>(n) * 16 <= kColsSmemMax) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(m / (16 / sizeof(T))));

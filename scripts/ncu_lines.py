@@ -33,3 +33,7 @@ print(f"total instructions {tot_i}, samples {tot_s}")
 print("-- by stall samples")
 for (fn, ln), (ie, ws, src) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
     print(f"{fn[:14]:14s}{ln:5d} {ie:9d} {ws:6d}  {src.strip()[:80]}")
+if len(sys.argv) > 4 and sys.argv[4] == "instr":
+    print("-- by instructions")
+    for (fn, ln), (ie, ws, src) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+        print(f"{fn[:14]:14s}{ln:5d} {ie:9d} {ws:6d}  {src.strip()[:80]}")

@@ -218,6 +218,27 @@ def test_large_vector_ball():
         np.testing.assert_allclose(mp.project_ball(v, q, r), O.project_ball(v, q, r), rtol=1e-10, atol=1e-13)
 
 
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("n,m", [(1000, 64), (2000, 48), (4096, 24), (8000, 12), (8193, 8), (3000, 6), (1, 32),
+                                 (7, 4), (4095, 40)])
+def test_l11_register_and_staged_geometries(dt, n, m):
+    """Every K3b l1 route: register strips of 16P-byte row pieces (P = 8, 4,
+    2, 1 by n), the shared-memory quad strip (n > 8192) and the column
+    kernels (m not a multiple of 4); mixed column scales so strips hold
+    zeroed, projected and (p = 2) shrunk columns; tie-heavy integer data."""
+    rng = np.random.default_rng(n * 7 + m)
+    scale = np.exp(rng.normal(size=m) * 1.5)
+    for kind in ("normal", "ties"):
+        if kind == "normal":
+            y = (rng.normal(size=(n, m)) * scale).astype(dt)
+        else:
+            y = (rng.integers(-3, 4, size=(n, m)) * np.round(scale * 4)).astype(dt)
+        for p, rel in (("1", 0.05), ("1", 0.3), ("2", 0.5)):
+            eta = rel * O.matrix_pq_norm(y.astype(np.float64), p, "1")
+            x, b, z = run(y, eta, p, "1")
+            check_bilevel(x, y, oracle_bilevel(y, eta, p, "1"), "1", zero_cols_gpu=z)
+
+
 def test_l11_unstaged_tall_columns():
     """n beyond the cluster's shared-memory capacity: unstaged strip path."""
     y = datagen.normal(14, (60000, 40))
