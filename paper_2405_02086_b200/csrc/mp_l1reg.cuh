@@ -16,9 +16,11 @@
 //    runs over registers with full ILP; per pass a warp reduce-scatter and
 //    one CTA barrier; the column lanes of every warp total the warp partials
 //    in warp order (deterministic, identical in every warp);
-//  * the apply shrinks the registers and stores the row pieces: no re-read.
-// (A grid-stride variant prefetching the next strip into shared memory with
-// cp.async measured slower: 283 vs 256 us on config 3.)
+//  * the apply shrinks the registers and stores the row pieces: no re-read;
+//  * PERSIST (default): one CTA per SM walks strips grid-stride and streams
+//    the next strip's row piece into each register right after storing it,
+//    so the loads overlap the apply (a cp.async prefetch into shared memory
+//    measured slower: 283 vs 256 us on config 3).
 //
 // Passes come in two kinds.  FAST (f32 strips, far from convergence): f32
 // per-thread sums (an f32->f64 convert per element would cost more than the
@@ -142,11 +144,11 @@ __device__ __forceinline__ uint4 reg_pack(const T (&e)[16 / sizeof(T)]) {
   }
 }
 
-template <typename T, int P, bool DERIVE>
+template <typename T, int P, bool DERIVE, bool PERSIST>
 __global__ void __launch_bounds__(kRegThreads, 1)
     k_l1reg(const T* __restrict__ y, T* __restrict__ x, int n, int64_t m, const double* __restrict__ v,
             const double* __restrict__ u, double* __restrict__ tau_out, const mp_info* __restrict__ info,
-            const OuterParams* __restrict__ params, double* __restrict__ u_out) {
+            const OuterParams* __restrict__ params, double* __restrict__ u_out, int64_t nstrips) {
   constexpr int C4 = 16 / sizeof(T);
   constexpr int W = C4 * P;  // strip columns
   constexpr int NT = kRegThreads;
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(kRegThreads, 1)
   constexpr int RPT = kRegRPT;
   constexpr bool kF32 = sizeof(T) == 4;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t strip = blockIdx.x;
+  int64_t strip = blockIdx.x;
   const int pc = (tid % P) * C4;  // this thread's first strip column
   const int rb = tid / P;         // this thread's first row
   const int64_t step = static_cast<int64_t>(SL) * m;
@@ -174,8 +176,9 @@ __global__ void __launch_bounds__(kRegThreads, 1)
 
   __shared__ FastPart wf[2][NW][W];
   __shared__ RegPart<T> wx[2][NW][W];
-  int npass = 0;
-  {
+  int npass = 0, nx = 0, nst = 0;
+  for (;;) {
+    ++nst;
     const int64_t cb = strip * W + pc;
     // this thread's columns: kinds (2 bits each: 1 feasible, 2 zero budget,
     // 3 project), live bits, thresholds
@@ -210,6 +213,7 @@ __global__ void __launch_bounds__(kRegThreads, 1)
       bool xp = !kF32;  // exact pass (CTA-uniform)
       for (int par = 0, it = 0; it < 4 * 1024; par ^= 1, ++it) {
         ++npass;
+        nx += xp;
         if (!xp) {
           FastPart a[C4];
 #pragma unroll
@@ -309,19 +313,24 @@ __global__ void __launch_bounds__(kRegThreads, 1)
 #pragma unroll
     for (int c = 0; c < C4; ++c) need_store = need_store || ((kinds >> (2 * c)) & 3u) == 2u;
     need_store = __syncthreads_or(need_store);
-    if (need_store) {
-      double t[C4];
-      TauPair tp[C4];
+    // PERSIST: stream the next strip into each register right after its
+    // store, so its loads overlap this strip's apply
+    const int64_t next = strip + gridDim.x;
+    const bool more = PERSIST && next < nstrips;
+    double t[C4];
+    TauPair tp[C4];
 #pragma unroll
-      for (int c = 0; c < C4; ++c) {
-        t[c] = __shfl_sync(0xffffffffu, td, pc + c);
-        tp[c].hi = __double2float_rn(t[c]);
-        tp[c].lo = __double2float_rn(t[c] - static_cast<double>(tp[c].hi));
-      }
-      T* xq = x + static_cast<int64_t>(rb) * m + cb;
+    for (int c = 0; c < C4; ++c) {
+      t[c] = __shfl_sync(0xffffffffu, td, pc + c);
+      tp[c].hi = __double2float_rn(t[c]);
+      tp[c].lo = __double2float_rn(t[c] - static_cast<double>(tp[c].hi));
+    }
+    T* xq = x + static_cast<int64_t>(rb) * m + cb;
+    const T* yn = y + static_cast<int64_t>(rb) * m + next * W + pc;
 #pragma unroll
-      for (int i = 0; i < RPT; ++i, xq += step) {
-        if (rb + SL * i >= n) break;
+    for (int i = 0; i < RPT; ++i, xq += step, yn += step) {
+      if (rb + SL * i >= n) break;
+      if (need_store) {
         T e[C4];
         reg_unpack<T>(q[i], e);
 #pragma unroll
@@ -340,12 +349,16 @@ __global__ void __launch_bounds__(kRegThreads, 1)
         }
         __stcs(reinterpret_cast<uint4*>(xq), reg_pack<T>(e));
       }
+      if (more) q[i] = __ldg(reinterpret_cast<const uint4*>(yn));
     }
+    if (!more) break;
+    strip = next;
   }
-  if (tid == 0 && g_mp_timeline) {  // profiling aid: passes, slots 8..10
+  if (tid == 0 && g_mp_timeline) {  // profiling aid: passes, max per CTA, strips, exact passes (8..11)
     atomicAdd(g_mp_timeline + 8, static_cast<unsigned long long>(npass));
+    atomicAdd(g_mp_timeline + 11, static_cast<unsigned long long>(nx));
     atomicMax(g_mp_timeline + 9, static_cast<unsigned long long>(npass));
-    atomicAdd(g_mp_timeline + 10, 1ull);
+    atomicAdd(g_mp_timeline + 10, static_cast<unsigned long long>(nst));
   }
   tl_end(3);
 }

@@ -287,6 +287,15 @@ inline bool l1reg_disabled() {
   return d;
 }
 
+// MP_L1REG_PERSIST=0: one CTA per strip instead of grid-stride (tuning aid).
+inline bool l1reg_persist() {
+  static const bool d = [] {
+    const char* e = std::getenv("MP_L1REG_PERSIST");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
+  return d;
+}
+
 // MP_L1REG_P=1|2|4|8 caps the register path's pieces per row (tuning aid).
 inline int l1reg_prefer_p() {
   static const int p = [] {
@@ -309,11 +318,23 @@ cudaError_t launch_reg(const T* y, T* x, int64_t n, int64_t m, const double* v, 
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  const int64_t nstrips = m / W;
+  if (l1reg_persist()) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(nstrips, sms)));
+    if (dv.params)
+      return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, true, true>, y, x, static_cast<int>(n), m, v, u, ws.tau, info,
+                                dv.params, dv.u_out, nstrips);
+    return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, false, true>, y, x, static_cast<int>(n), m, v, u, ws.tau, info,
+                              dv.params, dv.u_out, nstrips);
+  }
   if (dv.params)
-    return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, true>, y, x, static_cast<int>(n), m, v, u, ws.tau, info, dv.params,
-                              dv.u_out);
-  return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, false>, y, x, static_cast<int>(n), m, v, u, ws.tau, info, dv.params,
-                            dv.u_out);
+    return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, true, false>, y, x, static_cast<int>(n), m, v, u, ws.tau, info,
+                              dv.params, dv.u_out, nstrips);
+  return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, false, false>, y, x, static_cast<int>(n), m, v, u, ws.tau, info,
+                            dv.params, dv.u_out, nstrips);
 }
 
 template <typename T>

@@ -50,9 +50,8 @@ for rel in [float(r) for r in os.environ.get("RELS", "0.001,0.5").split(",")]:
         res.append(rel_t + [e0.elapsed_time(e1) * 1e3])
         extra = t[8:15]
     if extra[2] > 0:
-        print(f"  l1: mean passes {extra[0] / extra[2]:.2f} max {extra[1]:.0f} over {extra[2]:.0f} CTAs/columns;"
-              f" per-unit SM cycles: stage {extra[3] / extra[2]:.0f}  michelot {extra[4] / extra[2]:.0f}"
-              f"  apply {extra[5] / extra[2]:.0f}  (first pass {extra[6] / extra[2]:.0f})")
+        print(f"  l1: mean passes {extra[0] / extra[2]:.2f} per strip ({extra[3] / extra[2]:.2f} exact) over"
+              f" {extra[2]:.0f} strips; max per CTA {extra[1]:.0f}; aux slots {extra[4]:.0f} {extra[5]:.0f} {extra[6]:.0f}")
     inf_ = p.info()
     print(f"  info: iterations={inf_.iterations} survivors={inf_.survivors} zero_columns={inf_.zero_columns}")
     r = np.median(np.array(res), axis=0)
