@@ -374,3 +374,170 @@ int64_t orc_structured_sparsity(const double* x, int64_t n, int64_t m,
   }
   return count;
 }
+
+/* ---------------------------------------------------------------------------
+ * Exact Euclidean l_{1,inf} projection (proj/src/euclidean.cpp:82-170).
+ *
+ * Column j, magnitudes sorted descending a_1 >= ... >= a_n, long double
+ * prefix P_k = a_1 + ... + a_k; theta-space breakpoints t_k = P_k - k a_k
+ * (rounded to double, non-decreasing in k) and the column's total mass P_n
+ * (:28-49).  For theta below P_n the column's budget is
+ * u_j(theta) = (P_k - theta) / k with k = #{t_k <= theta} (at least 1,
+ * :19-26,51-61).  The optimal theta solves sum_j u_j(theta) = eta: the
+ * candidates are 0, every t_k and every P_n, sorted and deduplicated
+ * (:103-112); a bisection finds the first candidate whose budget sum is
+ * <= eta (:114-123) and the bracketing linear segment is solved exactly from
+ * the segment indices at its midpoint (:125-141).  Budgets are clamped at 0
+ * and X clips every column at its budget (:143-156).
+ */
+typedef struct {
+  double* mags;       /* descending */
+  long double* pref;  /* pref[k] = a_1 + ... + a_k, k = 0..n */
+  double* brk;        /* t_k, k = 1..n at brk[k-1] */
+  double total;
+} orc_col;
+
+static int desc_dbl(const void* a, const void* b) {
+  const double x = *(const double*)a, y = *(const double*)b;
+  return (x < y) - (x > y);
+}
+static int asc_dbl(const void* a, const void* b) {
+  const double x = *(const double*)a, y = *(const double*)b;
+  return (x > y) - (x < y);
+}
+
+/* upper_bound over the non-decreasing breakpoints: #{t_k <= theta} */
+static int64_t col_segment(const orc_col* c, int64_t n, double theta) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (c->brk[mid] <= theta) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+static double col_budget(const orc_col* c, double theta, int64_t k) {
+  return (double)((c->pref[k] - (long double)theta) / (long double)k);
+}
+
+static double budget_sum(const orc_col* cols, int64_t m, int64_t n, double theta) {
+  long double s = 0.0L;
+  for (int64_t j = 0; j < m; ++j) {
+    if (theta >= cols[j].total) continue;
+    int64_t k = col_segment(&cols[j], n, theta);
+    if (k == 0) k = 1;
+    s += col_budget(&cols[j], theta, k);
+  }
+  return (double)s;
+}
+
+int orc_euclid_l1inf(const double* y, int64_t n, int64_t m, double eta, double* x, double* budgets,
+                     double* theta_out) {
+  if (!radius_ok(eta)) return ORC_VALUE;
+  if (!all_finite(y, n * m)) return ORC_VALUE;
+  orc_col* cols = (orc_col*)calloc((size_t)(m > 0 ? m : 1), sizeof(orc_col));
+  double l1inf = 0.0;
+  for (int64_t j = 0; j < m; ++j) {
+    orc_col* c = &cols[j];
+    c->mags = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    c->pref = (long double*)malloc(sizeof(long double) * (size_t)(n + 1));
+    c->brk = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; ++i) c->mags[i] = fabs(y[i * m + j]);
+    qsort(c->mags, (size_t)n, sizeof(double), desc_dbl);
+    c->pref[0] = 0.0L;
+    for (int64_t k = 1; k <= n; ++k) {
+      c->pref[k] = c->pref[k - 1] + c->mags[k - 1];
+      c->brk[k - 1] = (double)(c->pref[k] - (long double)k * c->mags[k - 1]);
+    }
+    c->total = (double)c->pref[n];
+    l1inf += n > 0 ? c->mags[0] : 0.0;
+  }
+  int rc = ORC_OK;
+  double theta = 0.0;
+  if (l1inf <= eta) {
+    for (int64_t j = 0; j < m; ++j) budgets[j] = cols[j].mags[0];
+    memcpy(x, y, sizeof(double) * (size_t)(n * m));
+    theta = 0.0;
+    goto done;
+  }
+  if (eta == 0.0) {
+    for (int64_t j = 0; j < m; ++j) {
+      budgets[j] = 0.0;
+      if (cols[j].total > theta) theta = cols[j].total;
+    }
+    for (int64_t e = 0; e < n * m; ++e) x[e] = 0.0;
+    goto done;
+  }
+  {
+    const int64_t nb_max = m * (n + 1) + 1;
+    double* br = (double*)malloc(sizeof(double) * (size_t)nb_max);
+    int64_t nb = 0;
+    br[nb++] = 0.0;
+    for (int64_t j = 0; j < m; ++j) {
+      for (int64_t k = 0; k < n; ++k) br[nb++] = cols[j].brk[k];
+      br[nb++] = cols[j].total;
+    }
+    qsort(br, (size_t)nb, sizeof(double), asc_dbl);
+    int64_t u = 0;
+    for (int64_t i = 0; i < nb; ++i)
+      if (u == 0 || br[i] != br[u - 1]) br[u++] = br[i];
+    nb = u;
+    int64_t lo = 0, hi = nb - 1;
+    while (hi - lo > 1) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (budget_sum(cols, m, n, br[mid]) <= eta) hi = mid;
+      else lo = mid;
+    }
+    if (budget_sum(cols, m, n, br[hi]) == eta) {
+      theta = br[hi];
+    } else {
+      const double probe = 0.5 * (br[lo] + br[hi]);
+      long double a = 0.0L, b = 0.0L;
+      for (int64_t j = 0; j < m; ++j) {
+        if (probe >= cols[j].total) continue;
+        int64_t k = col_segment(&cols[j], n, probe);
+        if (k == 0) k = 1;
+        a += cols[j].pref[k] / (long double)k;
+        b += 1.0L / (long double)k;
+      }
+      theta = (double)((a - (long double)eta) / b);
+      if (theta < br[lo]) theta = br[lo];
+      if (theta > br[hi]) theta = br[hi];
+    }
+    free(br);
+  }
+  for (int64_t j = 0; j < m; ++j) {
+    budgets[j] = 0.0;
+    if (theta >= cols[j].total) continue;
+    int64_t k = col_segment(&cols[j], n, theta);
+    if (k == 0) k = 1;
+    const double b = col_budget(&cols[j], theta, k);
+    budgets[j] = b > 0.0 ? b : 0.0;
+  }
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < m; ++j) {
+      const double e = y[i * m + j];
+      x[i * m + j] = fabs(e) > budgets[j] ? copysign(budgets[j], e) : e;
+    }
+done:
+  if (theta_out) *theta_out = theta;
+  for (int64_t j = 0; j < m; ++j) {
+    free(cols[j].mags);
+    free(cols[j].pref);
+    free(cols[j].brk);
+  }
+  free(cols);
+  return rc;
+}
+
+/* clip_cost (proj/src/euclidean.cpp:64-80): sum_j sum_i max(|y_ij| - u_j, 0)^2. */
+double orc_clip_cost(const double* y, int64_t n, int64_t m, const double* budgets) {
+  double cost = 0.0;
+  for (int64_t j = 0; j < m; ++j)
+    for (int64_t i = 0; i < n; ++i) {
+      const double over = fabs(y[i * m + j]) - budgets[j];
+      if (over > 0.0) cost += over * over;
+    }
+  return cost;
+}

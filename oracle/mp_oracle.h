@@ -73,6 +73,15 @@ int orc_multilevel_norm(const double* t, const int64_t* shape, int order,
 int64_t orc_structured_sparsity(const double* x, int64_t n, int64_t m,
                                 double tol);
 
+/* Exact Euclidean l_{1,inf} projection (proj/src/euclidean.cpp:82-170):
+ * x (n, m) row-major, budgets[m], theta.  ORC_VALUE on a bad radius or
+ * non-finite data. */
+int orc_euclid_l1inf(const double* y, int64_t n, int64_t m, double eta, double* x, double* budgets,
+                     double* theta);
+
+/* clip_cost (proj/src/euclidean.cpp:64-80). */
+double orc_clip_cost(const double* y, int64_t n, int64_t m, const double* budgets);
+
 #ifdef __cplusplus
 }
 #endif

@@ -86,6 +86,10 @@ def lib():
         L.orc_project_fibers.restype = None
         L.orc_structured_sparsity.argtypes = [_P_D, C.c_int64, C.c_int64, C.c_double]
         L.orc_structured_sparsity.restype = C.c_int64
+        L.orc_euclid_l1inf.argtypes = [_P_D, C.c_int64, C.c_int64, C.c_double, _P_D, _P_D, C.POINTER(C.c_double)]
+        L.orc_euclid_l1inf.restype = C.c_int
+        L.orc_clip_cost.argtypes = [_P_D, C.c_int64, C.c_int64, _P_D]
+        L.orc_clip_cost.restype = C.c_double
         _lib = L
     return _lib
 
@@ -123,6 +127,13 @@ def ref():
         R.ref_gen_normal.restype = None
         R.ref_gen_raw.argtypes = [C.c_uint64, _P_U64, C.c_int64]
         R.ref_gen_raw.restype = None
+        R.ref_euclid.argtypes = [_P_D, C.c_int64, C.c_int64, C.c_double, _P_D, _P_D, C.POINTER(C.c_double)]
+        R.ref_euclid.restype = C.c_int
+        R.ref_budget_grid.argtypes = [_P_D, C.c_int64, C.c_int64, C.c_double, C.c_int64, _P_D,
+                                      C.POINTER(C.c_double)]
+        R.ref_budget_grid.restype = C.c_int
+        R.ref_clip_cost.argtypes = [_P_D, C.c_int64, C.c_int64, _P_D]
+        R.ref_clip_cost.restype = C.c_double
         _ref = R
     return _ref
 
@@ -227,6 +238,47 @@ def structured_sparsity(x, tol=0.0) -> int:
 
 
 # --------------------------------------------------------- compiled reference
+def euclid(y, eta):
+    """Exact Euclidean l1,inf projection (proj/src/euclidean.cpp:82-170):
+    returns (X, budgets, theta)."""
+    y = _d(y)
+    n, m = y.shape
+    x = np.empty_like(y)
+    b = np.empty(m)
+    th = C.c_double()
+    _check(lib().orc_euclid_l1inf(y, n, m, float(eta), x, b, C.byref(th)))
+    return x, b, th.value
+
+
+def clip_cost(y, budgets) -> float:
+    y = _d(y)
+    return float(lib().orc_clip_cost(y, y.shape[0], y.shape[1], _d(budgets)))
+
+
+def ref_euclid(y, eta):
+    y = _d(y)
+    n, m = y.shape
+    x = np.empty_like(y)
+    b = np.empty(m)
+    th = C.c_double()
+    _check(ref().ref_euclid(y, n, m, float(eta), x, b, C.byref(th)))
+    return x, b, th.value
+
+
+def ref_budget_grid(y, eta, steps):
+    y = _d(y)
+    n, m = y.shape
+    b = np.empty(m)
+    th = C.c_double()
+    _check(ref().ref_budget_grid(y, n, m, float(eta), int(steps), b, C.byref(th)))
+    return b, th.value
+
+
+def ref_clip_cost(y, budgets) -> float:
+    y = _d(y)
+    return float(ref().ref_clip_cost(y, y.shape[0], y.shape[1], _d(budgets)))
+
+
 def ref_bilevel(y, eta, p="1", q="inf", workers=1):
     y = _d(y)
     n, m = y.shape

@@ -17,6 +17,7 @@
 
 #include "multiproj/bilevel.hpp"
 #include "multiproj/errors.hpp"
+#include "multiproj/euclidean.hpp"
 #include "multiproj/multilevel.hpp"
 #include "multiproj/parallel.hpp"
 #include "multiproj/rng.hpp"
@@ -92,6 +93,32 @@ int ref_time_bilevel(const float* y32, int64_t n, int64_t m, int p, int q,
         (void)res;
       }
   });
+}
+
+// euclid_project_l1inf (proj/src/euclidean.cpp:82-170).
+int ref_euclid(const double* y, int64_t n, int64_t m, double eta, double* x, double* budgets, double* theta) {
+  return guarded([&] {
+    DenseTensor t({static_cast<size_t>(n), static_cast<size_t>(m)}, std::vector<double>(y, y + n * m));
+    EuclidResult r = euclid_project_l1inf(t, eta);
+    std::memcpy(x, r.X.data().data(), sizeof(double) * n * m);
+    std::memcpy(budgets, r.sol.budgets.data(), sizeof(double) * m);
+    *theta = r.sol.theta;
+  });
+}
+
+// budget_oracle_grid / clip_cost (proj/src/euclidean.cpp:64-80,172-240).
+int ref_budget_grid(const double* y, int64_t n, int64_t m, double eta, int64_t steps, double* budgets, double* theta) {
+  return guarded([&] {
+    DenseTensor t({static_cast<size_t>(n), static_cast<size_t>(m)}, std::vector<double>(y, y + n * m));
+    ColumnBudgetSolution s = budget_oracle_grid(t, eta, static_cast<std::size_t>(steps));
+    std::memcpy(budgets, s.budgets.data(), sizeof(double) * m);
+    *theta = s.theta;
+  });
+}
+
+double ref_clip_cost(const double* y, int64_t n, int64_t m, const double* budgets) {
+  DenseTensor t({static_cast<size_t>(n), static_cast<size_t>(m)}, std::vector<double>(y, y + n * m));
+  return clip_cost(t, std::span<const double>(budgets, static_cast<size_t>(m)));
 }
 
 int ref_multilevel(const double* t, const int64_t* shape, int order,

@@ -8,7 +8,8 @@ has compiled oracle/_ref/libmultiproj_ref.so from the reference sources:
 The fixtures are small seeded cases (inputs are fp32-representable so the
 fp32 device path consumes exactly the same values) covering every
 (p, q) pair, eta = 0, feasible inputs, ties, zero columns, ragged shapes and
-multi-level specs of order 1-4.  Outputs are the reference's own f64 results.
+multi-level specs of order 1-4, and the exact Euclidean l1,inf projection.
+Outputs are the reference's own f64 results.
 """
 from __future__ import annotations
 
@@ -92,9 +93,31 @@ def main():
     out["rng_raw_seed7"] = O.ref_gen_raw(7, 64)
     out["rng_uniform_seed2"] = O.ref_gen_uniform(2, 64, -1.0, 1.0)
     out["rng_normal_seed1"] = O.ref_gen_normal(1, 64)
+    # ---- exact Euclidean l1,inf (proj/src/euclidean.cpp), worked examples of
+    # proj/tests/test_euclidean.cpp:20-48 first
+    ecases = [(f32([[1, 0.5], [1, 0]]), 1.0, None), (f32([[0.3, 0.1], [-0.2, 0.05]]), 2.0, None),
+              (f32([[1, 2], [3, 4]]), 0.0, None)]
+    for shape in [(1, 1), (2, 3), (5, 1), (4, 4), (9, 7), (40, 24), (33, 130), (300, 17)]:
+        for rel in [0.0, 0.05, 0.3, 0.7, 0.99, 1.2]:
+            y = f32(rng.normal(size=shape))
+            if rng.uniform() < 0.3:  # ties and zero columns
+                y = f32(np.round(y * 2) / 2)
+                y[:, rng.integers(0, shape[1])] = 0.0
+            ecases.append((y, None, rel))
+    for i, (y, eta, rel) in enumerate(ecases):
+        if eta is None:
+            eta = rel * float(np.abs(y).max(axis=0).sum())
+        x, b, th = O.ref_euclid(y, eta)
+        out[f"eu{i}_y"] = y.astype(np.float32)
+        out[f"eu{i}_eta"] = np.array([eta])
+        out[f"eu{i}_x"] = x
+        out[f"eu{i}_b"] = b
+        out[f"eu{i}_theta"] = np.array([th])
+    out["eu_count"] = np.array([len(ecases)])
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
     np.savez_compressed(path, **out)
-    print(f"wrote {path}: {len(cases)} bilevel, {len(mcases)} multilevel, {len(vcases)} vector cases, "
+    print(f"wrote {path}: {len(cases)} bilevel, {len(mcases)} multilevel, {len(vcases)} vector, "
+          f"{len(ecases)} euclid cases, "
           f"{os.path.getsize(path) / 1024:.0f} KiB")
 
 

@@ -126,6 +126,50 @@ def test_golden_vector_balls(golden):
         assert bit_equal(O.project_ball(y, int(q), r), golden[f"vb{i}_x"]), i
 
 
+def test_golden_euclid(golden):  # proj/src/euclidean.cpp, fixtures from the compiled reference
+    for i in range(int(golden["eu_count"][0])):
+        y = golden[f"eu{i}_y"].astype(np.float64)
+        x, b, th = O.euclid(y, float(golden[f"eu{i}_eta"][0]))
+        assert bit_equal(x, golden[f"eu{i}_x"]), i
+        assert bit_equal(b, golden[f"eu{i}_b"]), i
+        assert th == golden[f"eu{i}_theta"][0], i
+
+
+def test_euclid_worked_example():  # proj/tests/test_euclidean.cpp:20-34
+    y = np.array([[1, 0.5], [1, 0]], float)
+    x, b, th = O.euclid(y, 1.0)
+    assert abs(th - 1 / 3) < 1e-12 and abs(b[0] - 5 / 6) < 1e-12 and abs(b[1] - 1 / 6) < 1e-12
+    assert abs(((y - x) ** 2).sum() - 1 / 6) < 1e-12
+    assert abs(((y - O.bilevel(y, 1.0)["X"]) ** 2).sum() - 0.1875) < 1e-12
+
+
+def test_euclid_identity_zero_and_errors():  # proj/tests/test_euclidean.cpp:36-55
+    y = np.array([[0.3, 0.1], [-0.2, 0.05]])
+    x, b, th = O.euclid(y, 2.0)
+    assert bit_equal(x, y) and th == 0.0
+    x, b, th = O.euclid(np.array([[1.0, 2], [3, 4]]), 0.0)
+    assert not x.any()
+    with pytest.raises(O.OracleError):
+        O.euclid(y, -1.0)
+
+
+def test_euclid_kkt_and_never_worse_than_bilevel():  # proj/tests/test_euclidean.cpp:77-125
+    rng = np.random.default_rng(43)
+    for _ in range(100):
+        n, m = (int(v) for v in rng.integers(2, 10, 2))
+        y = rng.normal(size=(n, m))
+        nrm = np.abs(y).max(axis=0).sum()
+        eta = rng.uniform(0.05, 0.95) * nrm
+        x, b, th = O.euclid(y, eta)
+        assert th > 0.0
+        resid = np.maximum(np.abs(y) - b[None, :], 0.0).sum(axis=0)
+        act = b > 0
+        np.testing.assert_allclose(resid[act], th, rtol=1e-9)
+        assert np.all(resid[~act] <= th * (1 + 1e-9) + 1e-12)
+        assert np.abs(x).max(axis=0).sum() <= eta * (1 + 1e-9) + 1e-15
+        assert ((y - x) ** 2).sum() <= ((y - O.bilevel(y, eta)["X"]) ** 2).sum() + 1e-12
+
+
 # --------------------------------------------- direct comparison with _ref
 needs_ref = pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
 
@@ -179,3 +223,32 @@ def test_trilevel_equals_reshaped_bilevel():
         x = O.ref_trilevel(t, eta)
         xb = O.bilevel(t.reshape(int(d[0] * d[1]), int(d[2])), eta)["X"].reshape(t.shape)
         assert bit_equal(x, xb)
+
+
+@needs_ref
+def test_restatement_matches_reference_euclid():
+    rng = np.random.default_rng(81)
+    for _ in range(300):
+        n, m = (int(v) for v in rng.integers(1, 14, 2))
+        y = rng.normal(size=(n, m))
+        if rng.uniform() < 0.3:
+            y = np.round(y * 2) / 2  # ties
+        eta = rng.uniform() * 1.2 * np.abs(y).max(axis=0).sum()
+        a, b = O.euclid(y, eta), O.ref_euclid(y, eta)
+        assert bit_equal(a[0], b[0]) and bit_equal(a[1], b[1]) and a[2] == b[2]
+
+
+@needs_ref
+def test_euclid_matches_budget_grid():  # proj/tests/test_euclidean.cpp:57-75
+    rng = np.random.default_rng(41)
+    for _ in range(30):
+        n, m = int(rng.integers(1, 6)), int(rng.integers(1, 4))
+        y = rng.uniform(-1, 1, (n, m))
+        nrm = np.abs(y).max(axis=0).sum()
+        eta = (0.2 + 0.7 * rng.uniform()) * nrm
+        steps = 2000 if m == 3 else 10000
+        x, b, th = O.euclid(y, eta)
+        gb, _ = O.ref_budget_grid(y, eta, steps)
+        assert ((y - x) ** 2).sum() <= O.ref_clip_cost(y, gb) + 1e-9
+        assert abs(O.clip_cost(y, gb) - O.ref_clip_cost(y, gb)) <= 1e-15 * max(1.0, O.clip_cost(y, gb))
+        assert np.all(np.abs(b - gb) <= 2 * eta / steps + 1e-9)
