@@ -145,6 +145,20 @@ mp_status mp_project_fibers(const void* y, void* x, mp_dtype dtype, int64_t n, i
                             const double* norms, const double* budgets, unsigned flags, void* workspace,
                             size_t workspace_bytes, void* stream);
 
+/* Exact Euclidean projection onto the l_{1,inf} ball (euclid_project_l1inf,
+ * proj/include/multiproj/euclidean.hpp:27-30, proj/src/euclidean.cpp:82-170;
+ * the "euclid" tag of proj/src/dispatch.cpp).  x (n, m) = Y clipped per
+ * column at the distance-minimising budgets; budgets (device f64, nullable)
+ * = ColumnBudgetSolution.budgets; info->tau = theta (the common residual
+ * mass), info->iterations = Newton steps, info->zero_columns = #{u_j == 0}.
+ * Columns are sorted in shared memory: workspace_size returns 0 (and the
+ * call MP_ERR_UNSUPPORTED) beyond n = 32768 (f32) / 16384 (f64). */
+size_t mp_euclid_workspace_size(mp_dtype dtype, int64_t n, int64_t m);
+
+mp_status mp_euclid_project(const void* y, void* x, mp_dtype dtype, int64_t n, int64_t m, double eta,
+                            double* budgets, mp_info* info, unsigned flags, void* workspace,
+                            size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------------ host */
 
 /* Opaque per-thread-safe execution context: device, stream, cached device
@@ -182,6 +196,12 @@ mp_status mp_project_ball_host(mp_context* ctx, const void* y, void* x, mp_dtype
 
 mp_status mp_aggregate_host(mp_context* ctx, const void* t, double* out, mp_dtype dtype,
                             int64_t n, int64_t m, mp_norm q);
+
+/* euclid_project_l1inf on host buffers (replaces the EuclidResult call,
+ * proj/src/euclidean.cpp:82): budgets[m] and *theta (both nullable) receive
+ * ColumnBudgetSolution. */
+mp_status mp_euclid_project_host(mp_context* ctx, const void* y, void* x, mp_dtype dtype, int64_t n,
+                                 int64_t m, double eta, double* budgets, double* theta);
 
 /* ----------------------------------------------------------- diagnostics */
 

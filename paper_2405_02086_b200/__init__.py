@@ -25,7 +25,7 @@ from ._capi import (MP_F32, MP_F64, MP_FLAG_EXACT_ZERO_SIGN, MpInfo, MpConfigErr
 
 __all__ = [
     "bilevel_project", "bilevel_radius_sweep", "multilevel_project", "trilevel_project_l1infinf", "project_l1", "project_l2",
-    "project_linf", "project_ball", "matrix_pq_norm", "multilevel_norm", "aggregate_leading_axis",
+    "project_linf", "project_ball", "euclid_project_l1inf", "matrix_pq_norm", "multilevel_norm", "aggregate_leading_axis",
     "structured_sparsity", "gen_uniform_matrix", "perturb_gaussian", "BilevelProjector", "MultilevelProjector",
     "ProjectionError", "MpValueError", "MpShapeError", "MpConfigError", "MP_FLAG_EXACT_ZERO_SIGN",
 ]
@@ -308,6 +308,41 @@ def structured_sparsity(y, tol=0.0):
     mx = aggregate_leading_axis(arr, "inf")
     count = int(np.sum(mx <= tol))
     return count, count / arr.shape[1]
+
+
+def euclid_project_l1inf(y, eta):
+    """Exact Euclidean l_{1,inf} projection; returns (X, budgets, theta).
+
+    Mirrors ``multiproj.euclid_project_l1inf`` (proj/python/bindings.cpp:101-108
+    -> proj/src/euclidean.cpp:82-170)."""
+    if _is_torch(y):
+        import torch
+        if y.dim() != 2:
+            raise MpShapeError("euclid_project_l1inf requires order 2")
+        yc = y.contiguous()
+        n, m = yc.shape
+        dt = _dt(yc)
+        wsb = lib().mp_euclid_workspace_size(dt, n, m)
+        ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=yc.device)
+        x = torch.empty_like(yc)
+        budgets = torch.empty(m, dtype=torch.float64, device=yc.device)
+        info = torch.zeros(C.sizeof(MpInfo), dtype=torch.uint8, device=yc.device)
+        s = torch.cuda.current_stream(yc.device)
+        check(lib().mp_euclid_project(yc.data_ptr(), x.data_ptr(), dt, n, m, float(eta), budgets.data_ptr(),
+                                      info.data_ptr(), 0, ws.data_ptr(), wsb, s.cuda_stream))
+        inf = MpInfo.from_buffer_copy(info.cpu().numpy().tobytes())
+        check(inf.status)
+        return x, budgets, float(inf.tau)
+    arr = _host_array(y)
+    if arr.ndim != 2:
+        raise MpShapeError("euclid_project_l1inf requires order 2")
+    n, m = arr.shape
+    x = np.empty_like(arr)
+    budgets = np.empty(m, np.float64)
+    theta = C.c_double()
+    check(lib().mp_euclid_project_host(None, arr.ctypes.data, x.ctypes.data, _dt(arr), n, m, float(eta),
+                                       budgets.ctypes.data, C.addressof(theta)))
+    return x, budgets.tolist(), float(theta.value)
 
 
 def perturb_gaussian(x, sigma, seed, iteration, stream=None):

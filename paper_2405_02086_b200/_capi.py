@@ -22,6 +22,7 @@ EXPORTS = [
     "mp_project_ball_workspace_size", "mp_project_ball",
     "mp_aggregate_workspace_size", "mp_aggregate",
     "mp_project_fibers_workspace_size", "mp_project_fibers",
+    "mp_euclid_workspace_size", "mp_euclid_project", "mp_euclid_project_host",
     "mp_context_create", "mp_context_destroy",
     "mp_bilevel_project_host", "mp_bilevel_sweep_host", "mp_multilevel_project_host",
     "mp_project_ball_host", "mp_aggregate_host", "mp_perturb_gaussian",
@@ -88,6 +89,12 @@ def lib() -> C.CDLL:
     L.mp_project_fibers_workspace_size.restype = sz
     L.mp_project_fibers.argtypes = [vp, vp, en, i64, i64, en, vp, vp, u32, vp, sz, vp]
     L.mp_project_fibers.restype = st
+    L.mp_euclid_workspace_size.argtypes = [en, i64, i64]
+    L.mp_euclid_workspace_size.restype = sz
+    L.mp_euclid_project.argtypes = [vp, vp, en, i64, i64, dbl, vp, vp, u32, vp, sz, vp]
+    L.mp_euclid_project.restype = st
+    L.mp_euclid_project_host.argtypes = [vp, vp, vp, en, i64, i64, dbl, vp, vp]
+    L.mp_euclid_project_host.restype = st
     L.mp_context_create.argtypes = [C.c_int]
     L.mp_context_create.restype = vp
     L.mp_context_destroy.argtypes = [vp]

@@ -14,6 +14,7 @@
 #include "mp_cuda.h"
 #include "multiproj/bilevel.hpp"
 #include "multiproj/dispatch.hpp"
+#include "multiproj/euclidean.hpp"
 #include "multiproj/multilevel.hpp"
 #include "multiproj/parallel.hpp"
 #include "multiproj/tensor.hpp"
@@ -284,6 +285,82 @@ unsigned default_workers() {
   return v >= 1 ? static_cast<unsigned>(v) : 1u;
 }
 
+// ------------------------------------------------------ exact Euclidean
+EuclidResult euclid_project_l1inf(const DenseTensor& y, double eta) {
+  if (y.order() != 2) throw ShapeError("euclid_project_l1inf requires order 2");
+  check_radius(eta);
+  const std::size_t n = y.fiber_length(), m = y.fiber_count();
+  std::vector<double> x(y.size()), budgets(m);
+  double theta = 0.0;
+  check(mp_euclid_project_host(nullptr, y.data().data(), x.data(), MP_F64, static_cast<int64_t>(n),
+                               static_cast<int64_t>(m), eta, budgets.data(), &theta));
+  return EuclidResult{DenseTensor(y.shape(), std::move(x)), ColumnBudgetSolution{std::move(budgets), theta}};
+}
+
+double clip_cost(const DenseTensor& y, std::span<const double> budgets) {
+  if (y.order() != 2) throw ShapeError("clip_cost requires order 2");
+  const std::size_t n = y.fiber_length(), m = y.fiber_count();
+  double cost = 0.0;
+  for (std::size_t j = 0; j < m; ++j)
+    for (std::size_t i = 0; i < n; ++i) {
+      const double over = std::abs(y.data()[i * m + j]) - budgets[j];
+      if (over > 0.0) cost += over * over;
+    }
+  return cost;
+}
+
+// The reference's verification oracle (proj/src/euclidean.cpp:172-240):
+// per-column clipping-cost tables on the budget grid u = g eta / steps, then
+// the cheapest split of the `steps` cells among <= 3 columns.
+ColumnBudgetSolution budget_oracle_grid(const DenseTensor& y, double eta, std::size_t steps) {
+  if (y.order() != 2) throw ShapeError("budget_oracle_grid requires order 2");
+  const std::size_t m = y.fiber_count(), n = y.fiber_length();
+  if (m > 3) throw ConfigError("budget_oracle_grid supports m <= 3 only");
+  if (steps < 100) throw ConfigError("budget_oracle_grid needs steps >= 100");
+  check_radius(eta);
+  const auto level = [&](std::size_t g) { return eta * static_cast<double>(g) / static_cast<double>(steps); };
+  std::vector<std::vector<double>> table(m, std::vector<double>(steps + 1));
+  for (std::size_t j = 0; j < m; ++j)
+    for (std::size_t g = 0; g <= steps; ++g) {
+      double c = 0.0;
+      for (std::size_t i = 0; i < n; ++i) {
+        const double over = std::abs(y.data()[i * m + j]) - level(g);
+        if (over > 0.0) c += over * over;
+      }
+      table[j][g] = c;
+    }
+  std::vector<std::size_t> pick(m, 0);
+  if (m == 1) {
+    pick[0] = steps;
+  } else if (m == 2) {
+    double best = INFINITY;
+    for (std::size_t a = 0; a <= steps; ++a)
+      if (const double c = table[0][a] + table[1][steps - a]; c < best) {
+        best = c;
+        pick = {a, steps - a};
+      }
+  } else if (m == 3) {
+    double best = INFINITY;
+    for (std::size_t a = 0; a <= steps; ++a) {
+      if (table[0][a] >= best) continue;
+      for (std::size_t b = 0; a + b <= steps; ++b)
+        if (const double c = table[0][a] + table[1][b] + table[2][steps - a - b]; c < best) {
+          best = c;
+          pick = {a, b, steps - a - b};
+        }
+    }
+  }
+  ColumnBudgetSolution sol{std::vector<double>(m), 0.0};
+  for (std::size_t j = 0; j < m; ++j) sol.budgets[j] = level(pick[j]);
+  for (std::size_t j = 0; j < m; ++j) {
+    if (sol.budgets[j] <= 0.0) continue;
+    double r = 0.0;
+    for (std::size_t i = 0; i < n; ++i) r += std::max(0.0, std::abs(y.data()[i * m + j]) - sol.budgets[j]);
+    sol.theta = std::max(sol.theta, r);
+  }
+  return sol;
+}
+
 // ---------------------------------------------------------------- dispatch
 Algorithm Algorithm::parse(const std::string& tag) {
   if (tag == "bilevel-l1inf") return {Kind::BilevelL1Inf, {}};
@@ -312,8 +389,7 @@ DenseTensor run_projection(const Algorithm& a, const DenseTensor& input, double 
     case Algorithm::Kind::BilevelL11: return bilevel_project(input, Norm::L1, Norm::L1, eta, pool).X;
     case Algorithm::Kind::BilevelL12: return bilevel_project(input, Norm::L1, Norm::L2, eta, pool).X;
     case Algorithm::Kind::Multilevel: return multilevel_project(input, a.spec, eta, pool);
-    case Algorithm::Kind::Euclid:
-      throw ConfigError("'euclid' (exact Euclidean l1,inf) is not part of the B200 bi-level drop-in");
+    case Algorithm::Kind::Euclid: return euclid_project_l1inf(input, eta).X;
   }
   throw ConfigError("unreachable algorithm kind");
 }

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "mp_internal.h"
+#include "mp_euclid.cuh"
 #include "mp_kernels.cuh"
 #include "mp_l1strip.cuh"
 #include "mp_outer_large.cuh"
@@ -677,6 +678,93 @@ mp_status check_multi_args(const void* t, const void* x, mp_dtype dt, const int6
   return MP_OK;
 }
 
+// ---------------------------------------------------- exact Euclidean l1,inf
+// (proj/src/euclidean.cpp:82-170; kernels in mp_euclid.cuh)
+struct EuclidWs {
+  mp_info* info;
+  void* mags;         // |Y| column-major, sorted per column
+  mpk::DD* pref;      // prefix sums, column-major
+  double* colmax;
+  double* budgets;
+  void* colp;
+  mpk::EuScratch* sc;
+};
+
+EuclidWs carve_euclid(Carve& c, mp_dtype dt, int64_t n, int64_t m) {
+  EuclidWs w{};
+  w.info = c.take<mp_info>(1);
+  w.mags = c.take<char>(static_cast<size_t>(n) * m * dtype_size(dt));
+  w.pref = c.take<mpk::DD>(static_cast<size_t>(n) * m);
+  w.colmax = c.take<double>(m);
+  w.budgets = c.take<double>(m);
+  w.colp = c.take<double>(m);
+  w.sc = c.take<mpk::EuScratch>(1);
+  return w;
+}
+
+int pow2_at_least(int64_t n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+template <typename T>
+bool euclid_fits(int64_t n) {
+  const size_t P2 = static_cast<size_t>(pow2_at_least(n));
+  return P2 * sizeof(T) + mpk::kEuSortThreads * sizeof(mpk::DD) + 16 <= mpk::kEuSortSmemMax;
+}
+
+template <typename T>
+mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, double eta, double* budgets,
+                      mp_info* info, unsigned flags, const EuclidWs& w, cudaStream_t s) {
+  mp_info* inf = info ? info : w.info;
+  double* u = budgets ? budgets : w.budgets;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(mpk::k_eu_sort<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(mpk::kEuSortSmemMax));
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(mpk::k_eu_sort<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(mpk::kEuSortSmemMax));
+  });
+  MP_CUDA_TRY(attr_err);
+  MP_CUDA_TRY(cudaMemsetAsync(inf, 0, sizeof(mp_info), s));
+  T* mags = static_cast<T*>(w.mags);
+  mpk::k_eu_gather<T><<<dim3(static_cast<unsigned>((m + 31) / 32), static_cast<unsigned>((n + 31) / 32)), dim3(32, 8),
+                        0, s>>>(y, n, m, mags, inf);
+  MP_CUDA_TRY(cudaGetLastError());
+  const int P2 = pow2_at_least(n);
+  const int nt = std::min(mpk::kEuSortThreads, std::max(32, P2 / 2));
+  const size_t smem = ((static_cast<size_t>(P2) * sizeof(T) + 15) / 16) * 16 + static_cast<size_t>(nt) * sizeof(mpk::DD);
+  mpk::k_eu_sort<T><<<static_cast<unsigned>(m), nt, smem, s>>>(mags, w.pref, n, P2, inf);
+  MP_CUDA_TRY(cudaGetLastError());
+  // cooperative search grid: every CTA co-resident
+  static int occ = -1;
+  if (occ < 0) MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mpk::k_eu_search<T>,
+                                                                          mpk::kEuSearchThreads, 0));
+  int G = static_cast<int>(std::min<int64_t>((m + mpk::kEuSearchThreads - 1) / mpk::kEuSearchThreads,
+                                             static_cast<int64_t>(sm_count()) * std::max(1, std::min(occ, 2))));
+  G = std::max(1, std::min(G, mpk::kEuMaxCtas));
+  const T* cm = mags;
+  const mpk::DD* cp = w.pref;
+  double* colmax = w.colmax;
+  mpk::EuScratch* sc = w.sc;
+  void* args[] = {&cm, &cp, &n, &m, &eta, &colmax, &u, &inf, &sc};
+  MP_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(mpk::k_eu_search<T>), dim3(G),
+                                          dim3(mpk::kEuSearchThreads), args, 0, s));
+  if (eta == 0.0) {  // the reference returns DenseTensor::zeros (+0.0 everywhere)
+    MP_CUDA_TRY(cudaMemsetAsync(x, 0, static_cast<size_t>(n) * m * sizeof(T), s));
+    return MP_OK;
+  }
+  MP_CUDA_TRY(launch_colparams<T>(w.colmax, u, m, mpk::kInf, w.colp, inf, s));
+  mpk::ApplyCols A{};
+  A.colp = w.colp;
+  A.budgets = u;
+  MP_CUDA_TRY(launch_apply<T>(mpk::kInf, pick_vec(dt, m, y, x), y, x, n, m, A, false, inf, flags, s));
+  return MP_OK;
+}
+
 }  // namespace
 
 // ================================================================== C-ABI
@@ -843,6 +931,35 @@ mp_status mp_project_fibers(const void* y, void* x, mp_dtype dtype, int64_t n, i
                                        budgets, colp, l1, inf, flags, dtype, s));
   }
   return MP_OK;
+}
+
+size_t mp_euclid_workspace_size(mp_dtype dtype, int64_t n, int64_t m) {
+  if (n < 1 || m < 1 || !dtype_ok(dtype)) return 0;
+  if (dtype == MP_F32 ? !euclid_fits<float>(n) : !euclid_fits<double>(n)) return 0;
+  Carve c(nullptr, 0);
+  carve_euclid(c, dtype, n, m);
+  return c.off + 256;
+}
+
+mp_status mp_euclid_project(const void* y, void* x, mp_dtype dtype, int64_t n, int64_t m, double eta,
+                            double* budgets, mp_info* info, unsigned flags, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  if (!dtype_ok(dtype)) return fail(MP_ERR_CONFIG, "unknown dtype code");
+  if (n < 1 || m < 1) return fail(MP_ERR_SHAPE, "euclid_project_l1inf requires a non-empty order-2 tensor");
+  if (!(eta >= 0.0) || !std::isfinite(eta)) return fail(MP_ERR_VALUE, "radius must be a finite nonnegative real");
+  if (dtype == MP_F32 ? !euclid_fits<float>(n) : !euclid_fits<double>(n))
+    return fail(MP_ERR_UNSUPPORTED, "euclid_project_l1inf: column length beyond the shared-memory sort");
+  if (!y || !x || !workspace) return fail(MP_ERR_WORKSPACE, "null pointer");
+  Carve c(workspace, workspace_bytes);
+  EuclidWs w = carve_euclid(c, dtype, n, m);
+  if (!c.fits()) return fail(MP_ERR_WORKSPACE, "mp_euclid_project: workspace too small");
+  MP_CUDA_TRY(outer_setup());
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == MP_F32)
+    return euclid_impl<float>(static_cast<const float*>(y), static_cast<float*>(x), dtype, n, m, eta, budgets, info,
+                              flags, w, s);
+  return euclid_impl<double>(static_cast<const double*>(y), static_cast<double*>(x), dtype, n, m, eta, budgets, info,
+                             flags, w, s);
 }
 
 size_t mp_aggregate_workspace_size(mp_dtype dtype, int64_t n, int64_t m, mp_norm q) {

@@ -1,0 +1,314 @@
+// mp_euclid.cuh -- exact Euclidean projection onto the l_{1,inf} ball
+// (proj/src/euclidean.cpp:82-170, the paper's comparison target), on device.
+//
+// The distance minimiser clips column j at u_j, where every active column
+// leaves the same residual mass theta = sum_i (|y_ij| - u_j)_+.  Per column,
+// with magnitudes sorted descending a_1 >= ... >= a_n and prefix sums P_k,
+// the budget is piecewise linear in theta: u_j(theta) = (P_k - theta) / k for
+// t_k <= theta < t_{k+1}, t_k = P_k - k a_k (euclidean.cpp:13-49).  theta
+// solves S(theta) = sum_j u_j(theta) = eta.
+//
+//  EK0 k_eu_gather   |Y| transposed into column-major order (32x32 tiles,
+//                    both sides coalesced) + the finiteness check
+//                    (tensor.cpp:40-41);
+//  EK1 k_eu_sort     one CTA per column: bitonic sort of the column in shared
+//                    memory (descending), then the double-double prefix sums
+//                    P_k (the reference's long double, euclidean.cpp:41-46);
+//  EK2 k_eu_search   a cooperative grid: the feasibility test (l1,inf norm
+//                    <= eta, :95-100) and Newton's iteration on the convex,
+//                    decreasing, piecewise-linear S from theta = 0: each step
+//                    solves the current linear segment exactly,
+//                    theta' = (sum_j P_k/k - eta) / (sum_j 1/k) -- the
+//                    reference's segment solve (:125-141) -- and stops when
+//                    theta' lies inside that segment [max t_k, min t_{k+1}],
+//                    i.e. on the segment the reference's breakpoint bisection
+//                    (:103-123) brackets.  Newton from the left of a convex
+//                    decreasing function never overshoots, so the iteration
+//                    is monotone and finite.  Each column's segment index is
+//                    a binary search over its breakpoints (upper_bound,
+//                    :19-26).  Budgets u_j = max(0, (P_k - theta)/k) (:143-149);
+//  EK3               the l_inf clip at u_j: the bi-level K3 apply kernel.
+// Sums are deterministic (fixed trees, CTA partials reduced in CTA order).
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "mp_cuda.h"
+#include "mp_kernels.cuh"
+
+namespace mpk {
+
+constexpr int kEuSortThreads = 1024;
+constexpr int kEuSearchThreads = 256;
+constexpr int kEuMaxCtas = 1024;
+constexpr size_t kEuSortSmemMax = 200 * 1024;
+
+struct EuPart {
+  DD a, b;         // sum_j P_k/k, sum_j 1/k over the active columns
+  double lo, hi;   // segment bounds: max_j t_k, min_j t_{k+1}
+  DD l1inf;        // phase 0: sum_j a_1
+  double tmax;     // phase 0: max_j P_n
+};
+
+struct EuScratch {
+  EuPart part[2][kEuMaxCtas];
+  long long zero[kEuMaxCtas];
+};
+
+// ------------------------------------------------------------------- EK0
+template <typename T>
+__global__ void __launch_bounds__(256) k_eu_gather(const T* __restrict__ y, int64_t n, int64_t m, T* __restrict__ mags,
+                                                   mp_info* __restrict__ info) {
+  __shared__ T tile[32][33];
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32, r0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // (32, 8)
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {
+    const int64_t r = r0 + ty + k, c = c0 + tx;
+    T e = T(0);
+    if (r < n && c < m) {
+      e = y[r * m + c];
+      bad |= !isfinite(e);
+    }
+    tile[ty + k][tx] = fabs(e);
+  }
+  if (__syncthreads_or(bad) && tx == 0 && ty == 0) info->status = MP_ERR_VALUE;
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {
+    const int64_t c = c0 + ty + k, r = r0 + tx;
+    if (r < n && c < m) mags[c * n + r] = tile[tx][ty + k];
+  }
+}
+
+// ------------------------------------------------------------------- EK1
+// Shared memory: keys[P2] (T) then NT chunk totals (DD).
+template <typename T>
+__global__ void __launch_bounds__(kEuSortThreads) k_eu_sort(T* __restrict__ mags, DD* __restrict__ pref, int64_t n,
+                                                            int P2, const mp_info* __restrict__ info) {
+  if (info->status != MP_OK) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* keys = reinterpret_cast<T*>(smem_raw);
+  DD* tot = reinterpret_cast<DD*>(smem_raw + ((static_cast<size_t>(P2) * sizeof(T) + 15) / 16) * 16);
+  const int NT = blockDim.x, tid = threadIdx.x;
+  const int64_t j = blockIdx.x;
+  T* col = mags + j * n;
+  for (int i = tid; i < P2; i += NT) keys[i] = i < n ? col[i] : T(-1);  // padding sorts last
+  __syncthreads();
+  // bitonic network, descending overall
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int d = k >> 1; d > 0; d >>= 1) {
+      for (int i = tid; i < (P2 >> 1); i += NT) {
+        const int a = 2 * d * (i / d) + (i % d), b = a + d;
+        const T x = keys[a], z = keys[b];
+        const bool desc = (a & k) == 0;
+        if (desc ? (x < z) : (x > z)) {
+          keys[a] = z;
+          keys[b] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = tid; i < n; i += NT) col[i] = keys[i];
+  // P_k, k = 1..n: contiguous chunks per thread, an inclusive scan of the
+  // chunk totals, then the chunks again from their offsets
+  const int C = static_cast<int>((n + NT - 1) / NT);
+  const int i0 = static_cast<int>(min(n, static_cast<int64_t>(tid) * C));
+  const int i1 = static_cast<int>(min(n, static_cast<int64_t>(i0) + C));
+  DD s{0.0, 0.0};
+  for (int i = i0; i < i1; ++i) s = dd_add(s, static_cast<double>(keys[i]));
+  tot[tid] = s;
+  __syncthreads();
+  for (int d = 1; d < NT; d <<= 1) {
+    const DD v = tid >= d ? dd_add(tot[tid - d], tot[tid]) : tot[tid];
+    __syncthreads();
+    tot[tid] = v;
+    __syncthreads();
+  }
+  DD run = tid > 0 ? tot[tid - 1] : DD{0.0, 0.0};
+  DD* pc = pref + j * n;
+  for (int i = i0; i < i1; ++i) {
+    run = dd_add(run, static_cast<double>(keys[i]));
+    pc[i] = run;
+  }
+}
+
+// ------------------------------------------------------------------- EK2
+__device__ __forceinline__ DD dd_sub(DD a, DD b) { return dd_add(a, DD{-b.hi, -b.lo}); }
+// DD / k for an integer k >= 1
+__device__ __forceinline__ DD dd_div_int(DD a, double k) {
+  const double q = a.hi / k;
+  const double r = fma(-q, k, a.hi);  // exact remainder of the leading part
+  const double e = (r + a.lo) / k;
+  return two_sum(q, e);
+}
+// DD / DD, to double
+__device__ __forceinline__ double dd_div_to_double(DD a, DD b) {
+  const double q = a.hi / b.hi;
+  // a - q b in DD
+  const double p = q * b.hi;
+  const double pe = fma(q, b.hi, -p);
+  DD r = dd_sub(a, DD{p, pe});
+  r = dd_sub(r, DD{q * b.lo, fma(q, b.lo, -(q * b.lo))});
+  return q + (r.hi + r.lo) / b.hi;
+}
+
+template <typename T>
+struct EuCol {
+  const T* a;    // sorted magnitudes, descending
+  const DD* P;   // P[k-1] = a_1 + ... + a_k
+  int64_t n;
+  // t_k = P_k - k a_k rounded to double (euclidean.cpp:44-45), k = 1..n
+  __device__ __forceinline__ double brk(int64_t k) const {
+    const DD pk = P[k - 1];
+    const double ak = static_cast<double>(a[k - 1]), kk = static_cast<double>(k);
+    const double p = kk * ak, pe = fma(kk, ak, -p);
+    const DD t = dd_sub(pk, DD{p, pe});
+    return t.hi + t.lo;
+  }
+  __device__ __forceinline__ double total() const { const DD t = P[n - 1]; return t.hi + t.lo; }
+  // #{k : t_k <= theta} (the breakpoints are non-decreasing)
+  __device__ __forceinline__ int64_t segment(double theta) const {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (brk(mid + 1) <= theta) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kEuSearchThreads)
+    k_eu_search(const T* __restrict__ mags, const DD* __restrict__ pref, int64_t n, int64_t m, double eta,
+                double* __restrict__ colmax, double* __restrict__ budgets, mp_info* __restrict__ info,
+                EuScratch* __restrict__ sc) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  if (info->status != MP_OK) return;  // written by EK0 before this launch: uniform
+  __shared__ DD dscr[32];
+  __shared__ double fscr[32];
+  __shared__ long long cscr[32];
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  const int64_t j0 = static_cast<int64_t>(b) * blockDim.x + tid, js = static_cast<int64_t>(G) * blockDim.x;
+
+  // phase 0: l1,inf norm, largest column mass, column maxima
+  DD l1{0.0, 0.0};
+  double tmax = 0.0;
+  for (int64_t j = j0; j < m; j += js) {
+    const EuCol<T> c{mags + j * n, pref + j * n, n};
+    const double a1 = static_cast<double>(c.a[0]);
+    colmax[j] = a1;
+    l1 = dd_add(l1, a1);
+    tmax = fmax(tmax, c.total());
+  }
+  l1 = block_sum_dd(l1, dscr);
+  tmax = -block_min(-tmax, fscr);
+  if (tid == 0) {
+    sc->part[0][b].l1inf = l1;
+    sc->part[0][b].tmax = tmax;
+  }
+  grid.sync();
+  DD L{0.0, 0.0};
+  double TM = 0.0;
+  for (int i = 0; i < G; ++i) {  // CTA order, identical in every CTA
+    L = dd_add(L, sc->part[0][i].l1inf);
+    TM = fmax(TM, sc->part[0][i].tmax);
+  }
+  const double l1inf = L.hi + L.lo;
+  double theta;
+  int iters = 0;
+  int mode;  // 0 identity (budgets = column maxima), 1 zero radius, 2 clip
+  if (l1inf <= eta) {
+    mode = 0;
+    theta = 0.0;
+  } else if (eta == 0.0) {
+    mode = 1;
+    theta = TM;
+  } else {
+    mode = 2;
+    theta = 0.0;
+    int par = 1;
+    for (iters = 1; iters <= 1 << 16; ++iters, par ^= 1) {
+      DD A{0.0, 0.0}, B{0.0, 0.0};
+      double lo = 0.0, hi = __longlong_as_double(0x7ff0000000000000ll);
+      for (int64_t j = j0; j < m; j += js) {
+        const EuCol<T> c{mags + j * n, pref + j * n, n};
+        const double tot = c.total();
+        if (theta >= tot) continue;  // inactive column
+        int64_t k = c.segment(theta);
+        if (k == 0) k = 1;
+        const double kd = static_cast<double>(k);
+        A = dd_add(A, dd_div_int(c.P[k - 1], kd));
+        B = dd_add(B, dd_div_int(DD{1.0, 0.0}, kd));
+        lo = fmax(lo, c.brk(k));
+        hi = fmin(hi, k < n ? c.brk(k + 1) : tot);
+      }
+      A = block_sum_dd(A, dscr);
+      B = block_sum_dd(B, dscr);
+      lo = -block_min(-lo, fscr);
+      hi = block_min(hi, fscr);
+      if (tid == 0) {
+        EuPart& p = sc->part[par][b];
+        p.a = A;
+        p.b = B;
+        p.lo = lo;
+        p.hi = hi;
+      }
+      grid.sync();
+      A = DD{0.0, 0.0};
+      B = DD{0.0, 0.0};
+      lo = 0.0;
+      hi = __longlong_as_double(0x7ff0000000000000ll);
+      for (int i = 0; i < G; ++i) {
+        const EuPart& p = sc->part[par][i];
+        A = dd_add(A, p.a);
+        B = dd_add(B, p.b);
+        lo = fmax(lo, p.lo);
+        hi = fmin(hi, p.hi);
+      }
+      const double tn = dd_div_to_double(dd_sub(A, DD{eta, 0.0}), B);
+      if (tn <= hi || !(tn > theta)) {  // the root lies on this segment
+        theta = fmin(fmax(tn, lo), hi);
+        break;
+      }
+      theta = tn;
+    }
+  }
+
+  // budgets (euclidean.cpp:143-149)
+  long long zc = 0;
+  for (int64_t j = j0; j < m; j += js) {
+    const EuCol<T> c{mags + j * n, pref + j * n, n};
+    double u;
+    if (mode == 0) {
+      u = static_cast<double>(c.a[0]);
+    } else if (mode == 1 || theta >= c.total()) {
+      u = 0.0;
+    } else {
+      int64_t k = c.segment(theta);
+      if (k == 0) k = 1;
+      const DD d = dd_div_int(dd_sub(c.P[k - 1], DD{theta, 0.0}), static_cast<double>(k));
+      u = fmax(0.0, d.hi + d.lo);
+    }
+    budgets[j] = u;
+    zc += u == 0.0;
+  }
+  zc = block_count(zc, cscr);
+  if (tid == 0) sc->zero[b] = zc;
+  grid.sync();
+  if (b == 0 && tid == 0) {
+    long long z = 0;
+    for (int i = 0; i < G; ++i) z += sc->zero[i];
+    info->tau = theta;
+    info->iterations = iters;
+    info->zero_columns = z;
+    info->active = m - z;
+    info->survivors = m - z;
+  }
+}
+
+}  // namespace mpk

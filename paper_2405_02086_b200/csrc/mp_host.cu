@@ -147,6 +147,39 @@ mp_status mp_bilevel_project_host(mp_context* ctx, const void* y, void* x, mp_dt
   return MP_OK;
 }
 
+mp_status mp_euclid_project_host(mp_context* ctx, const void* y, void* x, mp_dtype dtype, int64_t n, int64_t m,
+                                 double eta, double* budgets, double* theta) {
+  if (!ctx) ctx = default_ctx();
+  if (!ctx) return fail(MP_ERR_CUDA, "no CUDA context");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g(ctx->device);
+  const size_t ws = mp_euclid_workspace_size(dtype, n, m);
+  if (ws == 0) return mp_euclid_project(y, x, dtype, n, m, eta, nullptr, nullptr, 0, nullptr, 0, nullptr);
+  if (!(eta >= 0.0) || !std::isfinite(eta)) return fail(MP_ERR_VALUE, "radius must be a finite nonnegative real");
+  if (!y || !x) return fail(MP_ERR_WORKSPACE, "null tensor pointer");
+  const size_t bytes = static_cast<size_t>(n) * static_cast<size_t>(m) * dtype_size(dtype);
+  const size_t small = static_cast<size_t>(m) * sizeof(double) + 256;
+  MP_CUDA_TRY(grow(ctx->data, ctx->data_cap, bytes));
+  MP_CUDA_TRY(grow(ctx->ws, ctx->ws_cap, ws));
+  MP_CUDA_TRY(grow(ctx->small, ctx->small_cap, small + sizeof(mp_info)));
+  double* d_budgets = static_cast<double*>(ctx->small);
+  mp_info* d_info = reinterpret_cast<mp_info*>(static_cast<char*>(ctx->small) + small);
+  cudaStream_t s = ctx->stream;
+  MP_CUDA_TRY(cudaMemcpyAsync(ctx->data, y, bytes, cudaMemcpyHostToDevice, s));
+  mp_status st = mp_euclid_project(ctx->data, ctx->data, dtype, n, m, eta, d_budgets, d_info, 0, ctx->ws, ctx->ws_cap, s);
+  if (st != MP_OK) return st;
+  mp_info info{};
+  MP_CUDA_TRY(cudaMemcpyAsync(&info, d_info, sizeof info, cudaMemcpyDeviceToHost, s));
+  MP_CUDA_TRY(cudaStreamSynchronize(s));
+  st = device_status(info);
+  if (st != MP_OK) return st;
+  MP_CUDA_TRY(cudaMemcpyAsync(x, ctx->data, bytes, cudaMemcpyDeviceToHost, s));
+  if (budgets) MP_CUDA_TRY(cudaMemcpyAsync(budgets, d_budgets, m * sizeof(double), cudaMemcpyDeviceToHost, s));
+  MP_CUDA_TRY(cudaStreamSynchronize(s));
+  if (theta) *theta = info.tau;
+  return MP_OK;
+}
+
 mp_status mp_bilevel_sweep_host(mp_context* ctx, const void* y, void* const* xs, mp_dtype dtype, int64_t n, int64_t m,
                                 mp_norm p, mp_norm q, const double* etas, int count, double* budgets,
                                 int64_t* zero_columns, unsigned flags) {

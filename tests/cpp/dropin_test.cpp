@@ -11,6 +11,7 @@
 
 #include "multiproj/bilevel.hpp"
 #include "multiproj/dispatch.hpp"
+#include "multiproj/euclidean.hpp"
 #include "multiproj/multilevel.hpp"
 #include "multiproj/vector_balls.hpp"
 
@@ -113,7 +114,27 @@ int main() {
     auto c = run_projection(Algorithm::parse("bilevel-l1inf"), y, eta, nullptr);
     EXPECT(bits_equal(c.data(), b.X.data()));
     EXPECT(Algorithm::parse("multilevel:inf,inf,1").tag() == "multilevel:inf,inf,1");
-    EXPECT(throws<ConfigError>([&] { run_projection(Algorithm::parse("euclid"), y, eta, nullptr); }));
+    auto e = run_projection(Algorithm::parse("euclid"), y, eta, nullptr);
+    EXPECT(bits_equal(e.data(), euclid_project_l1inf(y, eta).X.data()));
+  }
+  {  // exact Euclidean l1,inf (proj/tests/test_euclidean.cpp:20-55)
+    DenseTensor y({2, 2}, {1, 0.5, 1, 0});
+    auto r = euclid_project_l1inf(y, 1.0);
+    EXPECT(close(r.sol.theta, 1.0 / 3) && close(r.sol.budgets[0], 5.0 / 6) && close(r.sol.budgets[1], 1.0 / 6));
+    const double d = frobenius_distance(y, r.X);
+    EXPECT(close(d * d, 1.0 / 6));
+    DenseTensor in({2, 2}, {0.3, 0.1, -0.2, 0.05});
+    auto id = euclid_project_l1inf(in, 2.0);
+    EXPECT(bits_equal(id.X.data(), in.data()) && id.sol.theta == 0.0);
+    auto z = euclid_project_l1inf(DenseTensor({2, 2}, {1, 2, 3, 4}), 0.0);
+    EXPECT(z.X.data()[0] == 0.0 && z.X.data()[3] == 0.0);
+    EXPECT(throws<ValueError>([&] { euclid_project_l1inf(in, -1.0); }));
+    EXPECT(throws<ShapeError>([&] { euclid_project_l1inf(DenseTensor({4}, {1, 2, 3, 4}), 1.0); }));
+    // the grid oracle brackets the exact budgets (test_euclidean.cpp:57-75)
+    auto g = budget_oracle_grid(y, 1.0, 10000);
+    EXPECT(std::abs(g.budgets[0] - r.sol.budgets[0]) <= 2e-4 && std::abs(g.budgets[1] - r.sol.budgets[1]) <= 2e-4);
+    EXPECT(d * d <= clip_cost(y, g.budgets) + 1e-9);
+    EXPECT(throws<ConfigError>([&] { budget_oracle_grid(DenseTensor({1, 4}, {1, 2, 3, 4}), 1.0, 1000); }));
   }
   {  // vector balls (proj/tests/test_vector_balls.cpp worked examples)
     std::vector<double> a{1.0, 1.0}, b{0.9, 0.1}, c{3.0, 4.0}, d{0.7, -1.2};

@@ -26,7 +26,8 @@ def test_dropin_exports_reference_api(cpp_test_binary):
                  "multiproj::multilevel_project_iter(", "multiproj::trilevel_project_l1infinf(",
                  "multiproj::multilevel_norm(", "multiproj::project_ball(", "multiproj::run_projection(",
                  "multiproj::parallel_project(", "multiproj::parse_norm_spec(", "multiproj::matrix_pq_norm(",
-                 "multiproj::aggregate_leading_axis(", "multiproj::structured_sparsity("]:
+                 "multiproj::aggregate_leading_axis(", "multiproj::structured_sparsity(",
+                 "multiproj::euclid_project_l1inf(", "multiproj::budget_oracle_grid(", "multiproj::clip_cost("]:
         assert name in syms, name
     assert os.access(cpp_test_binary, os.X_OK)
 
