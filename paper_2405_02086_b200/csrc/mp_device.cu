@@ -710,8 +710,19 @@ int pow2_at_least(int64_t n) {
 
 template <typename T>
 bool euclid_fits(int64_t n) {
-  const size_t P2 = static_cast<size_t>(pow2_at_least(n));
-  return P2 * sizeof(T) + mpk::kEuSortThreads * sizeof(mpk::DD) + 16 <= mpk::kEuSortSmemMax;
+  const size_t P2 = static_cast<size_t>(std::max(64, pow2_at_least(n)));
+  return P2 <= 32u * mpk::kEuSortThreads && P2 * sizeof(T) <= mpk::kEuSortSmemMax;
+}
+
+template <typename T, int E>
+cudaError_t launch_eu_sort(T* mags, mpk::DD* pref, int64_t n, int64_t m, int P2, int nt, size_t smem,
+                           const mp_info* inf, cudaStream_t s) {
+  static const cudaError_t attr = cudaFuncSetAttribute(mpk::k_eu_sort<T, E>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       static_cast<int>(mpk::kEuSortSmemMax));
+  if (attr != cudaSuccess) return attr;
+  mpk::k_eu_sort<T, E><<<static_cast<unsigned>(m), nt, smem, s>>>(mags, pref, n, P2, inf);
+  return cudaGetLastError();
 }
 
 template <typename T>
@@ -719,26 +730,24 @@ mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, doubl
                       mp_info* info, unsigned flags, const EuclidWs& w, cudaStream_t s) {
   mp_info* inf = info ? info : w.info;
   double* u = budgets ? budgets : w.budgets;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(mpk::k_eu_sort<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(mpk::kEuSortSmemMax));
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(mpk::k_eu_sort<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(mpk::kEuSortSmemMax));
-  });
-  MP_CUDA_TRY(attr_err);
   MP_CUDA_TRY(cudaMemsetAsync(inf, 0, sizeof(mp_info), s));
   T* mags = static_cast<T*>(w.mags);
   mpk::k_eu_gather<T><<<dim3(static_cast<unsigned>((m + 31) / 32), static_cast<unsigned>((n + 31) / 32)), dim3(32, 8),
                         0, s>>>(y, n, m, mags, inf);
   MP_CUDA_TRY(cudaGetLastError());
-  const int P2 = pow2_at_least(n);
-  const int nt = std::min(mpk::kEuSortThreads, std::max(32, P2 / 2));
-  const size_t smem = ((static_cast<size_t>(P2) * sizeof(T) + 15) / 16) * 16 + static_cast<size_t>(nt) * sizeof(mpk::DD);
-  mpk::k_eu_sort<T><<<static_cast<unsigned>(m), nt, smem, s>>>(mags, w.pref, n, P2, inf);
-  MP_CUDA_TRY(cudaGetLastError());
+  // 16 keys per thread (32 beyond 16384): most of the network runs in
+  // registers and shuffles; small columns keep one warp
+  const int P2 = std::max(64, pow2_at_least(n));
+  const int ek = P2 >= 512 ? std::max(16, P2 / mpk::kEuSortThreads) : P2 / 32;
+  const int nt = P2 / ek;
+  const size_t smem = static_cast<size_t>(P2) * sizeof(T);
+  switch (P2 / nt) {
+    case 2: MP_CUDA_TRY((launch_eu_sort<T, 2>(mags, w.pref, n, m, P2, nt, smem, inf, s))); break;
+    case 4: MP_CUDA_TRY((launch_eu_sort<T, 4>(mags, w.pref, n, m, P2, nt, smem, inf, s))); break;
+    case 8: MP_CUDA_TRY((launch_eu_sort<T, 8>(mags, w.pref, n, m, P2, nt, smem, inf, s))); break;
+    case 16: MP_CUDA_TRY((launch_eu_sort<T, 16>(mags, w.pref, n, m, P2, nt, smem, inf, s))); break;
+    default: MP_CUDA_TRY((launch_eu_sort<T, 32>(mags, w.pref, n, m, P2, nt, smem, inf, s))); break;
+  }
   // cooperative search grid: every CTA co-resident
   static int occ = -1;
   if (occ < 0) MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mpk::k_eu_search<T>,

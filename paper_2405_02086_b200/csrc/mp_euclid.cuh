@@ -11,9 +11,10 @@
 //  EK0 k_eu_gather   |Y| transposed into column-major order (32x32 tiles,
 //                    both sides coalesced) + the finiteness check
 //                    (tensor.cpp:40-41);
-//  EK1 k_eu_sort     one CTA per column: bitonic sort of the column in shared
-//                    memory (descending), then the double-double prefix sums
-//                    P_k (the reference's long double, euclidean.cpp:41-46);
+//  EK1 k_eu_sort     one CTA per column: bitonic sort (descending) in
+//                    registers / shuffles / shared memory, then the
+//                    double-double prefix sums P_k (the reference's long
+//                    double, euclidean.cpp:41-46);
 //  EK2 k_eu_search   a cooperative grid: the feasibility test (l1,inf norm
 //                    <= eta, :95-100) and Newton's iteration on the convex,
 //                    decreasing, piecewise-linear S from theta = 0: each step
@@ -83,55 +84,113 @@ __global__ void __launch_bounds__(256) k_eu_gather(const T* __restrict__ y, int6
 }
 
 // ------------------------------------------------------------------- EK1
-// Shared memory: keys[P2] (T) then NT chunk totals (DD).
+// Bitonic sort, descending, of P2 = NT * E keys: thread t holds keys
+// t*E .. t*E+E-1 in registers.  Partner distance d < E: inside the thread;
+// d < 32E: the same register of lane ^ (d/E), by shuffle; larger d: one
+// shared-memory round trip in an [E][NT] layout (conflict-free).  Then the
+// double-double prefix sums P_k (the reference's long double,
+// euclidean.cpp:41-46) over the thread-contiguous chunks: a block scan of the
+// chunk totals and one more pass over the registers.
 template <typename T>
+__device__ __forceinline__ void bitonic_keep(T& v, T o, bool take_max) {
+  v = take_max ? (v > o ? v : o) : (v < o ? v : o);
+}
+
+template <typename T, int E>
 __global__ void __launch_bounds__(kEuSortThreads) k_eu_sort(T* __restrict__ mags, DD* __restrict__ pref, int64_t n,
                                                             int P2, const mp_info* __restrict__ info) {
   if (info->status != MP_OK) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* keys = reinterpret_cast<T*>(smem_raw);
-  DD* tot = reinterpret_cast<DD*>(smem_raw + ((static_cast<size_t>(P2) * sizeof(T) + 15) / 16) * 16);
-  const int NT = blockDim.x, tid = threadIdx.x;
+  T* sk = reinterpret_cast<T*>(smem_raw);  // [E][NT]
+  __shared__ DD wsum[32];
+  const int NT = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t j = blockIdx.x;
   T* col = mags + j * n;
-  for (int i = tid; i < P2; i += NT) keys[i] = i < n ? col[i] : T(-1);  // padding sorts last
-  __syncthreads();
-  // bitonic network, descending overall
+  T v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = tid * E + e;
+    v[e] = i < n ? col[i] : T(-1);  // padding sorts last
+  }
   for (int k = 2; k <= P2; k <<= 1) {
-    for (int d = k >> 1; d > 0; d >>= 1) {
-      for (int i = tid; i < (P2 >> 1); i += NT) {
-        const int a = 2 * d * (i / d) + (i % d), b = a + d;
-        const T x = keys[a], z = keys[b];
-        const bool desc = (a & k) == 0;
-        if (desc ? (x < z) : (x > z)) {
-          keys[a] = z;
-          keys[b] = x;
-        }
+    int d = k >> 1;
+    for (; d >= 32 * E; d >>= 1) {  // shared memory
+#pragma unroll
+      for (int e = 0; e < E; ++e) sk[e * NT + tid] = v[e];
+      __syncthreads();
+      const int pt = tid ^ (d / E);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = tid * E + e;
+        const bool lower = tid < pt, desc = (i & k) == 0;
+        bitonic_keep(v[e], sk[e * NT + pt], lower == desc);
       }
       __syncthreads();
     }
+    for (; d >= E; d >>= 1) {  // shuffles
+      const int dl = d / E;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = tid * E + e;
+        const T o = __shfl_xor_sync(0xffffffffu, v[e], dl);
+        const bool lower = (lane & dl) == 0, desc = (i & k) == 0;
+        bitonic_keep(v[e], o, lower == desc);
+      }
+    }
+#pragma unroll
+    for (int dd = E / 2; dd >= 1; dd >>= 1) {  // registers
+      if (dd >= k) continue;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if (e & dd) continue;
+        const int i = tid * E + e;
+        const bool desc = (i & k) == 0;
+        const T a = v[e], b = v[e + dd];
+        const bool sw = desc ? (a < b) : (a > b);
+        v[e] = sw ? b : a;
+        v[e + dd] = sw ? a : b;
+      }
+    }
   }
-  for (int i = tid; i < n; i += NT) col[i] = keys[i];
-  // P_k, k = 1..n: contiguous chunks per thread, an inclusive scan of the
-  // chunk totals, then the chunks again from their offsets
-  const int C = static_cast<int>((n + NT - 1) / NT);
-  const int i0 = static_cast<int>(min(n, static_cast<int64_t>(tid) * C));
-  const int i1 = static_cast<int>(min(n, static_cast<int64_t>(i0) + C));
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = tid * E + e;
+    if (i < n) col[i] = v[e];
+  }
+  // prefix sums: chunk totals, warp scan, warp totals, block offsets
   DD s{0.0, 0.0};
-  for (int i = i0; i < i1; ++i) s = dd_add(s, static_cast<double>(keys[i]));
-  tot[tid] = s;
-  __syncthreads();
-  for (int d = 1; d < NT; d <<= 1) {
-    const DD v = tid >= d ? dd_add(tot[tid - d], tot[tid]) : tot[tid];
-    __syncthreads();
-    tot[tid] = v;
-    __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if (tid * E + e < n) s = dd_add(s, static_cast<double>(v[e]));
+  DD inc = s;  // inclusive warp scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const DD w{__shfl_up_sync(0xffffffffu, inc.hi, o), __shfl_up_sync(0xffffffffu, inc.lo, o)};
+    if (lane >= o) inc = dd_add(w, inc);
   }
-  DD run = tid > 0 ? tot[tid - 1] : DD{0.0, 0.0};
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    DD t = lane < (NT >> 5) ? wsum[lane] : DD{0.0, 0.0};
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const DD w{__shfl_up_sync(0xffffffffu, t.hi, o), __shfl_up_sync(0xffffffffu, t.lo, o)};
+      if (lane >= o) t = dd_add(w, t);
+    }
+    wsum[lane] = t;  // inclusive over warps
+  }
+  __syncthreads();
+  DD run = warp > 0 ? wsum[warp - 1] : DD{0.0, 0.0};
+  const DD ex{__shfl_up_sync(0xffffffffu, inc.hi, 1), __shfl_up_sync(0xffffffffu, inc.lo, 1)};
+  if (lane > 0) run = dd_add(run, ex);
   DD* pc = pref + j * n;
-  for (int i = i0; i < i1; ++i) {
-    run = dd_add(run, static_cast<double>(keys[i]));
-    pc[i] = run;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = tid * E + e;
+    if (i < n) {
+      run = dd_add(run, static_cast<double>(v[e]));
+      pc[i] = run;
+    }
   }
 }
 
