@@ -134,6 +134,15 @@ def ref():
         R.ref_budget_grid.restype = C.c_int
         R.ref_clip_cost.argtypes = [_P_D, C.c_int64, C.c_int64, _P_D]
         R.ref_clip_cost.restype = C.c_double
+        R.ref_write_uniform_tensor.argtypes = [C.c_char_p, _P_I64, C.c_int, C.c_uint64, C.c_double, C.c_double,
+                                               C.POINTER(C.c_uint64)]
+        R.ref_write_uniform_tensor.restype = C.c_int
+        R.ref_read_tensor_checksum.argtypes = [C.c_char_p, C.POINTER(C.c_uint64), C.POINTER(C.c_int64)]
+        R.ref_read_tensor_checksum.restype = C.c_int
+        R.ref_rng_stream.argtypes = [C.c_uint64, C.c_int, _P_U64, _P_D]
+        R.ref_rng_stream.restype = C.c_int
+        R.ref_write_records_sample.argtypes = [C.c_char_p]
+        R.ref_write_records_sample.restype = C.c_int
         _ref = R
     return _ref
 
@@ -277,6 +286,30 @@ def ref_budget_grid(y, eta, steps):
 def ref_clip_cost(y, budgets) -> float:
     y = _d(y)
     return float(ref().ref_clip_cost(y, y.shape[0], y.shape[1], _d(budgets)))
+
+
+def ref_write_uniform_tensor(path, shape, seed, lo=-1.0, hi=1.0) -> int:
+    sh = np.ascontiguousarray(shape, np.int64)
+    ck = C.c_uint64()
+    _check(ref().ref_write_uniform_tensor(str(path).encode(), sh, len(shape), seed, lo, hi, C.byref(ck)))
+    return ck.value
+
+
+def ref_read_tensor_checksum(path):
+    ck, sz = C.c_uint64(), C.c_int64()
+    _check(ref().ref_read_tensor_checksum(str(path).encode(), C.byref(ck), C.byref(sz)))
+    return ck.value, sz.value
+
+
+def ref_rng_stream(seed, count):
+    raw = np.empty(count, np.uint64)
+    nrm = np.empty(count)
+    _check(ref().ref_rng_stream(seed, count, raw, nrm))
+    return raw, nrm
+
+
+def ref_write_records_sample(path) -> None:
+    _check(ref().ref_write_records_sample(str(path).encode()))
 
 
 def ref_bilevel(y, eta, p="1", q="inf", workers=1):

@@ -16,7 +16,9 @@
 #include <vector>
 
 #include "multiproj/bilevel.hpp"
+#include "multiproj/bench.hpp"
 #include "multiproj/errors.hpp"
+#include "multiproj/tensor_io.hpp"
 #include "multiproj/euclidean.hpp"
 #include "multiproj/multilevel.hpp"
 #include "multiproj/parallel.hpp"
@@ -92,6 +94,57 @@ int ref_time_bilevel(const float* y32, int64_t n, int64_t m, int p, int q,
         times[idx++] = std::chrono::duration<double>(t1 - t0).count();
         (void)res;
       }
+  });
+}
+
+// Host formats / generator / records (proj/src/tensor_io.cpp, rng.cpp,
+// bench.cpp:200-266): the drop-in must read and write the same bytes.
+int ref_write_uniform_tensor(const char* path, const int64_t* shape, int order, uint64_t seed, double lo, double hi,
+                             uint64_t* checksum) {
+  return guarded([&] {
+    std::vector<size_t> sh(shape, shape + order);
+    DenseTensor t = gen_uniform_tensor(sh, seed, lo, hi);
+    write_tensor(t, path);
+    *checksum = tensor_checksum(t);
+  });
+}
+
+int ref_read_tensor_checksum(const char* path, uint64_t* checksum, int64_t* size) {
+  return guarded([&] {
+    DenseTensor t = read_tensor(path);
+    *checksum = tensor_checksum(t);
+    *size = static_cast<int64_t>(t.size());
+  });
+}
+
+int ref_rng_stream(uint64_t seed, int count, uint64_t* raw, double* normals) {
+  return guarded([&] {
+    Xoshiro256pp a(seed), b(seed);
+    for (int i = 0; i < count; ++i) raw[i] = a.next();
+    for (int i = 0; i < count; ++i) normals[i] = b.normal();
+  });
+}
+
+// Two records, one with a comma-carrying multilevel tag, through the
+// reference writer.
+int ref_write_records_sample(const char* path) {
+  return guarded([&] {
+    BenchRecord a;
+    a.algorithm = "bilevel-l1inf";
+    a.n = 10;
+    a.m = 20;
+    a.radius = 0.1;
+    a.workers = 4;
+    a.repetitions = 3;
+    a.median_seconds = 1.0 / 3.0;
+    a.achieved_norm = 0.1;
+    a.zero_columns = 7;
+    a.output_checksum = 0xfedcba9876543210ULL;
+    BenchRecord b = a;
+    b.algorithm = "multilevel:inf,inf,1";
+    b.extra_dims = {3, 5};
+    b.median_seconds = 2.5e-7;
+    write_csv_records({a, b}, path);
   });
 }
 

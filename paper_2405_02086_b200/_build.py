@@ -45,6 +45,14 @@ def build_cpp_test(out: str) -> str:
     return out
 
 
+def build_io_test(out: str) -> str:
+    """Compile tests/cpp/io_compat.cpp (host-side formats, no GPU calls)."""
+    src = os.path.join(ROOT, "tests", "cpp", "io_compat.cpp")
+    subprocess.run(["g++", "-std=c++20", "-O1", f"-I{INCLUDE}", src, f"-L{PKG}", "-lmultiproj_b200", "-lmp_b200",
+                    f"-Wl,-rpath,{PKG}", "-o", out], check=True)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> None:
     deps = glob.glob(os.path.join(CSRC, "*")) + [os.path.join(INCLUDE, "mp_cuda.h")]
     if force or _stale(LIB, deps):
@@ -54,10 +62,10 @@ def build(force: bool = False, verbose: bool = False) -> None:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
         os.replace(LIB + ".tmp", LIB)
-    di = os.path.join(CSRC, "dropin", "multiproj_dropin.cpp")
-    di_deps = [di, LIB] + glob.glob(os.path.join(INCLUDE, "multiproj", "*.hpp"))
+    di = [os.path.join(CSRC, "dropin", f) for f in ("multiproj_dropin.cpp", "multiproj_io.cpp")]
+    di_deps = di + [LIB] + glob.glob(os.path.join(INCLUDE, "multiproj", "*.hpp"))
     if force or _stale(DROPIN, di_deps):
-        subprocess.run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", f"-I{INCLUDE}", di, f"-L{PKG}", "-lmp_b200",
+        subprocess.run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", f"-I{INCLUDE}", *di, f"-L{PKG}", "-lmp_b200",
                         "-Wl,-rpath,$ORIGIN", "-o", DROPIN], check=True)
     dg = os.path.join(CSRC, "datagen.c")
     if force or _stale(DATAGEN, [dg]):

@@ -9,7 +9,15 @@
 #include <random>
 #include <vector>
 
+#include <unistd.h>
+
+#include <filesystem>
+#include <string>
+
+#include "multiproj/bench.hpp"
 #include "multiproj/bilevel.hpp"
+#include "multiproj/rng.hpp"
+#include "multiproj/tensor_io.hpp"
 #include "multiproj/dispatch.hpp"
 #include "multiproj/euclidean.hpp"
 #include "multiproj/multilevel.hpp"
@@ -147,6 +155,35 @@ int main() {
     auto pd = project_linf(d, 1.0);
     EXPECT(pd[0] == 0.7 && pd[1] == -1.0);
     EXPECT(throws<ValueError>([&] { project_ball(a, Norm::L1, -1.0); }));
+  }
+  {  // bench records and file projection (proj/tests/test_bench.cpp:20-146)
+    const std::string dir = std::filesystem::temp_directory_path() / ("mp_dropin_" + std::to_string(::getpid()));
+    std::filesystem::create_directories(dir);
+    auto recs = run_radius_sweep({"bilevel-l1inf", "bilevel-l11", "multilevel:inf,1"}, 40, 30, {0.5, 2.0}, 5, 2, 1);
+    EXPECT(recs.size() == 6);
+    for (const auto& r : recs) EXPECT(r.achieved_norm <= r.radius * (1 + 1e-9) && r.repetitions == 2 && r.n == 40);
+    write_csv_records(recs, dir + "/r.csv");
+    auto back = read_csv_records(dir + "/r.csv");
+    EXPECT(back.size() == recs.size() && back[4].algorithm == "multilevel:inf,1" &&
+           back[5].output_checksum == recs[5].output_checksum && back[2].median_seconds == recs[2].median_seconds);
+    auto sizes = run_size_sweep({"multilevel:inf,inf,1"}, {{6, 5, 4}}, 1.0, 9, 1, 1);
+    EXPECT(sizes.size() == 1 && sizes[0].extra_dims == std::vector<std::size_t>{4});
+    auto eu = run_size_sweep({"euclid", "bilevel-l12"}, {{6, 5}, {9, 3}}, 1.0, 9, 1, 1);
+    EXPECT(eu.size() == 4 && eu[0].achieved_norm <= 1.0 + 1e-9 && eu[3].m == 3);
+    auto sp = measure_speedup(Algorithm::parse("bilevel-l1inf"), {50, 40}, 1.0, {1, 2, 4}, 1);
+    EXPECT(sp.size() == 3 && sp[0].output_checksum == sp[2].output_checksum);
+    DenseTensor y = gen_uniform_matrix(20, 10, 3, -1.0, 1.0);
+    write_tensor(y, dir + "/in.mlpt");
+    write_tensor(y, dir + "/in.csv");
+    auto rep = project_file(dir + "/in.mlpt", dir + "/out.mlpt", Algorithm::parse("bilevel-l1inf"), 1.0, 1);
+    auto repc = project_file(dir + "/in.csv", dir + "/out.csv", Algorithm::parse("bilevel-l1inf"), 1.0, 1);
+    DenseTensor xo = read_tensor(dir + "/out.mlpt");
+    EXPECT(bits_equal(xo.data(), bilevel_project_l1inf(y, 1.0).X.data()));
+    EXPECT(bits_equal(read_tensor(dir + "/out.csv").data(), xo.data()));
+    EXPECT(rep.achieved_norm <= 1.0 * (1 + 1e-9) && rep.distance > 0 && repc.zero_columns == rep.zero_columns);
+    EXPECT(throws<ConfigError>([&] { project_file(dir + "/in.mlpt", dir + "/o.mlpt", Algorithm::parse("multilevel:inf,inf,1"), 1.0, 1); }));
+    EXPECT(throws<ConfigError>([&] { bench_one(Algorithm::parse("bilevel-l1inf"), y, 1.0, 0, 1); }));
+    std::filesystem::remove_all(dir);
   }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
