@@ -730,6 +730,7 @@ mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, doubl
                       mp_info* info, unsigned flags, const EuclidWs& w, cudaStream_t s) {
   mp_info* inf = info ? info : w.info;
   double* u = budgets ? budgets : w.budgets;
+  prof_mark(0, s);
   MP_CUDA_TRY(cudaMemsetAsync(inf, 0, sizeof(mp_info), s));
   T* mags = static_cast<T*>(w.mags);
   mpk::k_eu_gather<T><<<dim3(static_cast<unsigned>((m + 31) / 32), static_cast<unsigned>((n + 31) / 32)), dim3(32, 8),
@@ -764,13 +765,14 @@ mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, doubl
                                           dim3(mpk::kEuSearchThreads), args, 0, s));
   if (eta == 0.0) {  // the reference returns DenseTensor::zeros (+0.0 everywhere)
     MP_CUDA_TRY(cudaMemsetAsync(x, 0, static_cast<size_t>(n) * m * sizeof(T), s));
-    return MP_OK;
+  } else {
+    MP_CUDA_TRY(launch_colparams<T>(w.colmax, u, m, mpk::kInf, w.colp, inf, s));
+    mpk::ApplyCols A{};
+    A.colp = w.colp;
+    A.budgets = u;
+    MP_CUDA_TRY(launch_apply<T>(mpk::kInf, pick_vec(dt, m, y, x), y, x, n, m, A, false, inf, flags, s));
   }
-  MP_CUDA_TRY(launch_colparams<T>(w.colmax, u, m, mpk::kInf, w.colp, inf, s));
-  mpk::ApplyCols A{};
-  A.colp = w.colp;
-  A.budgets = u;
-  MP_CUDA_TRY(launch_apply<T>(mpk::kInf, pick_vec(dt, m, y, x), y, x, n, m, A, false, inf, flags, s));
+  prof_mark(3, s);
   return MP_OK;
 }
 

@@ -60,8 +60,8 @@ def timed_graph(call, nproj=1):
     return float(np.median(ts))
 
 
-def line(name, n_elems, f_surv, ms, cpu_s=None, extra=None):
-    b = 4.0 * n_elems * (2.0 + f_surv)
+def line(name, n_elems, f_surv, ms, cpu_s=None, extra=None, s=4.0):
+    b = s * n_elems * (2.0 + f_surv)
     d = {"config": name, "ms": ms, "algo_bytes": b, "GBps": b / (ms * 1e-3) / 1e9, "frac_measured_hbm": b / (ms * 1e-3) / 1e9 / peak,
          "f_surv": f_surv}
     if cpu_s is not None:
@@ -105,7 +105,16 @@ for rel in (0.001, 0.01, 0.1, 0.5):
     out["results"].append(line(f"c2 bilevel l1,inf 10000x10000 U[-1,1] eta={rel}", y.size,
                                p.info().survivors / y.shape[1], ms, cpu_bilevel(y, eta, "1", "inf") if rel in (0.001, 0.5) else None,
                                {"zero_columns": p.info().zero_columns}))
-del yd, xd
+# config 2 in f64 (the C++ drop-in's dtype, the reference's arithmetic)
+yd64 = yd.double()
+xd64 = torch.empty_like(yd64)
+p64 = mp.BilevelProjector(*y.shape, dtype="float64", device=dev)
+eta = 0.1 * float(colmax.sum())
+ms = timed_graph(lambda: p64(yd64, xd64, eta, stream=stream))
+p64(yd64, xd64, eta); torch.cuda.synchronize()
+out["results"].append(line("c2 f64 bilevel l1,inf 10000x10000 U[-1,1] eta=0.1", y.size, p64.info().survivors / y.shape[1],
+                           ms, None, {"zero_columns": p64.info().zero_columns}, s=8.0))
+del yd, xd, yd64, xd64
 
 # config 3 (l1,1 and l1,2)
 y = datagen.config_input(3)
@@ -137,6 +146,33 @@ if CPU and O.ref_available():
 out["results"].append(line("c4 trilevel l1,inf,inf 256^3 N(0,1) eta=0.05", t.size, mpj.info().survivors / t.shape[2], ms,
                            cpu_s))
 del td_, xd
+
+# exact Euclidean l1,inf at the config-1 and config-3 shapes
+for cfg, rel in ((1, 0.1), (3, 0.1)):
+    y = datagen.config_input(cfg)
+    n_, m_ = y.shape
+    eta = rel * float(np.abs(y).max(axis=0).astype(np.float64).sum())
+    yd = torch.from_numpy(y).to(dev)
+    xd = torch.empty_like(yd)
+    wsb = lib.mp_euclid_workspace_size(_capi.MP_F32, n_, m_)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    bd = torch.empty(m_, dtype=torch.float64, device=dev)
+    info = torch.zeros(C.sizeof(_capi.MpInfo), dtype=torch.uint8, device=dev)
+    call = lambda: _capi.check(lib.mp_euclid_project(yd.data_ptr(), xd.data_ptr(), _capi.MP_F32, n_, m_, eta,
+                                                     bd.data_ptr(), info.data_ptr(), 0, ws.data_ptr(), wsb,
+                                                     stream.cuda_stream))
+    ms = timed_graph(call)
+    inf = _capi.MpInfo.from_buffer_copy(info.cpu().numpy().tobytes())
+    cpu_s = None
+    if CPU and O.ref_available() and cfg == 1:
+        t0 = time.perf_counter()
+        O.ref_euclid(y.astype(np.float64), eta)
+        cpu_s = time.perf_counter() - t0
+    out["results"].append(line(f"euclid l1,inf {n_}x{m_} (config-{cfg} input) eta={rel}", y.size, 1.0, ms, cpu_s,
+                               {"newton_iterations": int(inf.iterations), "theta": inf.tau,
+                                "note": "algorithmic bytes as a bi-level projection (read + write); the sort "
+                                        "dominates, not HBM"}))
+    del yd, xd, ws
 
 # config 5 (loop of 100: perturb + project)
 y = datagen.config_input(5)
