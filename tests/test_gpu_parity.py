@@ -368,3 +368,42 @@ def test_radius_sweep_host_api_matches_single_calls():
         x1, b1, z1 = mp.bilevel_project(y, e)
         assert bit_equal(x, x1) and z == z1
         np.testing.assert_array_equal(np.asarray(b), np.asarray(b1))
+
+
+@pytest.mark.parametrize("q", ["inf", "2", "1"])
+def test_beyond_int32_element_count(q):
+    """40000 x 60000 (8192 x 300000 for l1,1) fp32, 2.4-2.5e9 elements
+    (> 2^31): 64-bit offsets end to end.
+    Inputs are generated on the device (torch); the checker is the oracle's
+    outer projection of exact column norms (torch.amax / float64 sums) and the
+    per-column apply on sampled columns."""
+    import torch
+    n, m = (8192, 300000) if q == "1" else (40000, 60000)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    y = torch.rand((n, m), generator=g, device="cuda", dtype=torch.float32).mul_(2).sub_(1)
+    if q == "inf":
+        v = y.abs().amax(dim=0).double().cpu().numpy()
+    elif q == "2":
+        v = torch.linalg.vector_norm(y.double(), dim=0).cpu().numpy()
+    else:
+        v = y.double().abs().sum(dim=0).cpu().numpy()
+    eta = 0.05 * float(v.sum())
+    proj = mp.BilevelProjector(n, m, "float32", "1", q)
+    x = proj(y, torch.empty_like(y), eta)
+    torch.cuda.synchronize()
+    inf = proj.info()
+    assert inf.status == 0
+    u_ref = O.project_ball(v, "1", eta)
+    u_gpu = proj.budgets.cpu().numpy()
+    np.testing.assert_allclose(u_gpu, u_ref, rtol=1e-9, atol=1e-12)
+    rng = np.random.default_rng(5)
+    cols = np.concatenate([[0, m - 1], rng.choice(m, 30, replace=False)])
+    yc = y[:, cols].double().cpu().numpy()
+    xc = x[:, cols].double().cpu().numpy()
+    ref = O.project_fibers(yc, q, v[cols], u_ref[cols])
+    if q == "1":
+        check_bilevel(xc, yc, {"X": ref, "v": v[cols], "tau": -1.0, "zero_columns": 0}, "1")
+    else:
+        np.testing.assert_allclose(xc, ref, rtol=1e-6, atol=1e-7)
+    del y, x
+    torch.cuda.empty_cache()
