@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <mutex>
@@ -64,6 +65,9 @@ namespace {
 
 // ----------------------------------------------------------- grid planning
 constexpr int kRowInterleave = 1;  // see mpk::row_walk: the grid sweeps HBM band by band
+// K1 row blocks hold >= 16 rows: short matrices otherwise pile one atomic /
+// partial per row onto every column (1000x1000: K1 9.9 -> 4.4 us); K3 keeps 4.
+constexpr int64_t kK1MinRows = 16;
 
 struct Grid {
   int vec = 1;
@@ -104,7 +108,7 @@ cudaError_t launch_pdl(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem,
 // 1.005-wave grid costs a whole extra CTA lifetime).  Each thread keeps U
 // 16-byte loads in flight; at full occupancy that is >= 128 KiB per SM, well
 // above the ~35 KiB Little's law asks of HBM3e.
-Grid plan_grid(int vec, int64_t n, int64_t m, int ctas_per_sm) {
+Grid plan_grid(int vec, int64_t n, int64_t m, int ctas_per_sm, int64_t min_rows = 4) {
   Grid g;
   g.vec = vec;
   g.threads = threads_for(vec, m);
@@ -112,7 +116,7 @@ Grid plan_grid(int vec, int64_t n, int64_t m, int ctas_per_sm) {
   g.ntiles = (slots + g.threads - 1) / g.threads;
   const int64_t resident = static_cast<int64_t>(sm_count()) * std::max(1, ctas_per_sm);
   int64_t nrb = std::max<int64_t>(1, resident / g.ntiles);
-  nrb = std::min<int64_t>(nrb, std::max<int64_t>(1, (n + 3) / 4));  // >= 4 rows per block
+  nrb = std::min<int64_t>(nrb, std::max<int64_t>(1, (n + min_rows - 1) / min_rows));
   nrb = std::min<int64_t>(nrb, 65535);
   g.rpb = (n + nrb - 1) / nrb;
   g.nrb = (n + g.rpb - 1) / g.rpb;
@@ -154,7 +158,7 @@ int64_t max_nrb(mp_dtype dt, int64_t n, int64_t m) {
   for (int v : {1, 2, 4, 8}) {
     if (dt == MP_F64 && v == 8) continue;
     const int t = threads_for(v, m);
-    r = std::max(r, plan_grid(v, n, m, std::min(32, 2048 / t)).nrb);
+    r = std::max(r, plan_grid(v, n, m, std::min(32, 2048 / t), kK1MinRows).nrb);
   }
   return r;
 }
@@ -178,7 +182,7 @@ cudaError_t launch_colnorm_rg(int64_t n, int64_t m, const T* y, void* out, Grid&
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessorWithFlags(&occ, fn, tx * ty, smem, 0) != cudaSuccess || occ < 1)
     occ = 1;
-  g = plan_grid(VEC, n, m, occ);  // g.nrb = CTA rows; row slots = g.nrb * ty
+  g = plan_grid(VEC, n, m, occ, kK1MinRows);  // g.nrb = CTA rows; row slots = g.nrb * ty
   const int64_t slots = g.nrb * ty;
   const int64_t rpb = kRowInterleave ? n / slots : (n + slots - 1) / slots;
   dim3 grid(static_cast<unsigned>(g.ntiles), static_cast<unsigned>(g.nrb));
@@ -285,14 +289,21 @@ cudaError_t launch_outer_p(const mpk::OuterArgs& a, int C, int chunk, cudaStream
   return cudaLaunchKernelEx(&cfg, mpk::k_outer<P>, a);
 }
 
-template <int P>
+template <int P, int NT = mpk::kOuterRegThreads>
 cudaError_t launch_outer_reg(const mpk::OuterArgs& a, cudaStream_t s) {
-  return launch_pdl(mpk::k_outer_reg<P>, dim3(1), dim3(mpk::kOuterRegThreads), 0, s, a);
+  return launch_pdl(mpk::k_outer_reg<P, NT>, dim3(1), dim3(NT), 0, s, a);
 }
 
 cudaError_t launch_outer(const mpk::OuterArgs& a, cudaStream_t s) {
   cudaError_t e = outer_setup();
   if (e != cudaSuccess) return e;
+  if (a.m <= 2048) {  // small vectors: a 256-thread CTA, cheaper barriers
+    const int64_t per = (std::max<int64_t>(a.m, 1) + 255) / 256;
+    if (per <= 1) return launch_outer_reg<1, 256>(a, s);
+    if (per <= 2) return launch_outer_reg<2, 256>(a, s);
+    if (per <= 4) return launch_outer_reg<4, 256>(a, s);
+    return launch_outer_reg<8, 256>(a, s);
+  }
   if (a.m <= mpk::kOuterRegMaxM) {
     const int64_t per = (std::max<int64_t>(a.m, 1) + mpk::kOuterRegThreads - 1) / mpk::kOuterRegThreads;
     if (per <= 1) return launch_outer_reg<1>(a, s);

@@ -721,12 +721,13 @@ constexpr int kOuterRegThreads = 1024;
 constexpr int kOuterRegMaxP = 12;
 constexpr int64_t kOuterRegMaxM = static_cast<int64_t>(kOuterRegThreads) * kOuterRegMaxP;
 
-// K2 fast path (m <= 16384): ONE CTA of 1024 threads, the vector held in
+// K2 fast path (m <= 12288): ONE CTA of NT threads (1024; 256 for m <= 2048,
+// where the barriers of the per-pass all-reduce dominate), the vector held in
 // registers (P per thread, compile time), every reduction a single-barrier
 // all-reduce.  The kernel's time is its dependency chain on one SM: a load
 // wave, 1 + passes + 1 block reductions, one double division per pass.
-template <int P>
-__global__ void __launch_bounds__(kOuterRegThreads, 1) k_outer_reg(OuterArgs a) {
+template <int P, int NT = kOuterRegThreads>
+__global__ void __launch_bounds__(NT, 1) k_outer_reg(OuterArgs a) {
   pdl_wait();
   pdl_trigger();
   tl_begin(2);
@@ -742,14 +743,14 @@ __global__ void __launch_bounds__(kOuterRegThreads, 1) k_outer_reg(OuterArgs a) 
   int bad = 0;
 #pragma unroll
   for (int j = 0; j < P; ++j) {
-    const int i = tid + j * kOuterRegThreads;
+    const int i = tid + j * NT;
     v[j] = (i < m) ? outer_load(a, i) : 0.0;
   }
   int nzero = 0;
 #pragma unroll
   for (int j = 0; j < P; ++j) {
     bad += !isfinite(v[j]);
-    nzero += (v[j] == 0.0) && (tid + j * kOuterRegThreads < m);
+    nzero += (v[j] == 0.0) && (tid + j * NT < m);
     s += (a.p == kL2) ? v[j] * v[j] : fabs(v[j]);
   }
   // one int channel: non-finite flag (bit 18+) and #{v == 0} (bits 0..17)
@@ -788,7 +789,7 @@ __global__ void __launch_bounds__(kOuterRegThreads, 1) k_outer_reg(OuterArgs a) 
       unsigned mask = 0;
 #pragma unroll
       for (int j = 0; j < P; ++j)
-        if (tid + j * kOuterRegThreads < m) mask |= 1u << j;
+        if (tid + j * NT < m) mask |= 1u << j;
       double t = (s - eta) / static_cast<double>(m);
       int kprev = m;
       double S = s;
@@ -824,7 +825,7 @@ __global__ void __launch_bounds__(kOuterRegThreads, 1) k_outer_reg(OuterArgs a) 
   if (a.emit) {
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-      const int i = tid + j * kOuterRegThreads;
+      const int i = tid + j * NT;
       if (i < m) {
         const double x = v[j];
         double u = x;
