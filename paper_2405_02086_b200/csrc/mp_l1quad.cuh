@@ -88,9 +88,7 @@ __global__ void __launch_bounds__(kQuadThreads)
     double S = 0.0;
     bool done = kind != 3;
     if (done) cnt = 0;
-    long long ckp1 = 0;
     for (int pass = 0; pass < 4 * 1024; ++pass) {
-      if (pass == 1) ckp1 = clock64();
       ++npass;
       const T thr = round_down_to(T(0), t);
       // Batches of 8: all loads first (independent LDS in flight), then the
@@ -154,7 +152,6 @@ __global__ void __launch_bounds__(kQuadThreads)
       }
       if (!__syncthreads_or(!done)) break;
     }
-    if (threadIdx.x == 0 && g_mp_timeline && ckp1) atomicAdd(g_mp_timeline + 14, static_cast<unsigned long long>(ckp1 - ck1));
     if (kind == 3 && g == 0 && k == 0) stau[c] = (S - uj) / static_cast<double>(K);
     __syncthreads();
   }
