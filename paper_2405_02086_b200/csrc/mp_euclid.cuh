@@ -92,8 +92,20 @@ __global__ void __launch_bounds__(256) k_eu_gather(const T* __restrict__ y, int6
 // euclidean.cpp:41-46) over the thread-contiguous chunks: a block scan of the
 // chunk totals and one more pass over the registers.
 template <typename T>
+__device__ __forceinline__ T tmax(T a, T b) {
+  if constexpr (sizeof(T) == 4) return fmaxf(a, b);
+  else return fmax(a, b);
+}
+template <typename T>
+__device__ __forceinline__ T tmin(T a, T b) {
+  if constexpr (sizeof(T) == 4) return fminf(a, b);
+  else return fmin(a, b);
+}
+// keys are finite and >= -1 (padding): min / max are branch-free selects
+template <typename T>
 __device__ __forceinline__ void bitonic_keep(T& v, T o, bool take_max) {
-  v = take_max ? (v > o ? v : o) : (v < o ? v : o);
+  const T hi = tmax(v, o), lo = tmin(v, o);
+  v = take_max ? hi : lo;
 }
 
 template <typename T, int E>
@@ -145,10 +157,9 @@ __global__ void __launch_bounds__(kEuSortThreads) k_eu_sort(T* __restrict__ mags
         if (e & dd) continue;
         const int i = tid * E + e;
         const bool desc = (i & k) == 0;
-        const T a = v[e], b = v[e + dd];
-        const bool sw = desc ? (a < b) : (a > b);
-        v[e] = sw ? b : a;
-        v[e + dd] = sw ? a : b;
+        const T hi = tmax(v[e], v[e + dd]), lo = tmin(v[e], v[e + dd]);
+        v[e] = desc ? hi : lo;
+        v[e + dd] = desc ? lo : hi;
       }
     }
   }
