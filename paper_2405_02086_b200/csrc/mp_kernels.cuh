@@ -932,6 +932,17 @@ __global__ void __launch_bounds__(kThreads)
       dead = dead && (A.budgets[c0 + j] == 0.0);
     }
   }
+  // Zero-budget packs are stored without a read, but only when the whole
+  // 8-lane group (128 contiguous bytes) is zero-budget: a line half written
+  // early by a read-free pack and half late by a loading one is evicted
+  // partially valid and costs a DRAM read-modify-write (f64 l_inf with 37%
+  // zero columns: K3 410 -> 174 us at 4096x16384).  Lanes past m count as dead.
+  {
+    const int lane = threadIdx.x & 31;
+    const unsigned grp = 0xffu << (lane & ~7);
+    const unsigned db = __ballot_sync(__activemask(), dead) | ~__activemask();
+    dead = (db & grp) == grp;
+  }
   if (rw.cnt <= 0) return;
   // This CTA's rows are swept LAST-FIRST: K1 swept them first-last in the
   // same resident wave, so the rows it touched last are still in L2 when
@@ -949,6 +960,8 @@ __global__ void __launch_bounds__(kThreads)
   }
   auto op = [&](T e, int j) -> T {
     if constexpr (Q == kInf) {
+      // a zero budget inside a live group: copysign keeps y's zero sign,
+      // the reference's bytes (read-free groups write +0.0; +-0 compare equal)
       if constexpr (sizeof(T) == 4) return fabsf(e) > rd[j] ? copysignf(rn[j], e) : e;
       else return fabs(e) > pu[j] ? copysign(pu[j], e) : e;
     } else {

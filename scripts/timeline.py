@@ -16,10 +16,11 @@ n = int(os.environ.get("N", "10000"))
 m = int(os.environ.get("M", str(n)))
 q = os.environ.get("Q", "inf")
 y_h = datagen.normal(3, (n, m)) if os.environ.get("DIST") == "normal" else datagen.uniform(2, (n, m), -1.0, 1.0)
-y = torch.from_numpy(y_h).cuda()
+DT = os.environ.get("DT", "float32")
+y = torch.from_numpy(y_h).cuda().to(getattr(torch, DT))
 x = torch.empty_like(y)
 colmax = np.abs(y_h).max(axis=0).astype(np.float64)
-p = mp.BilevelProjector(n, m, "float32", "1", q)
+p = mp.BilevelProjector(n, m, DT, "1", q)
 flush_buf = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
 tl = torch.empty(16, dtype=torch.int64, device="cuda")
 s = torch.cuda.Stream()

@@ -201,9 +201,10 @@ def test_ragged_and_unaligned():
             check_bilevel(x, y, oracle_bilevel(y, eta, "1", q), q, zero_cols_gpu=z)
 
 
-@pytest.mark.parametrize("m", [2049, 9999, 70000, 130000])
+@pytest.mark.parametrize("m", [2049, 9999, 16384, 24576, 70000, 130000])
 def test_wide_outer_cluster_and_cooperative(m):
-    """K2 on 1..16-CTA clusters (m <= 98304) and as a cooperative grid beyond."""
+    """K2: one CTA (registers, or shared memory up to m = 24576), 1..16-CTA
+    clusters (m <= 98304) and a cooperative grid beyond."""
     y = datagen.normal(12, (3, m))
     for q in NORMS:
         eta = 0.05 * O.matrix_pq_norm(y.astype(np.float64), "1", q)
