@@ -186,6 +186,20 @@ mp_status mp_bilevel_sweep_host(mp_context* ctx, const void* y, void* const* xs,
                                 int64_t m, mp_norm p, mp_norm q, const double* etas, int count,
                                 double* budgets, int64_t* zero_columns, unsigned flags);
 
+/* The same sweep, enqueued and returned from at once (a serving pipeline over
+ * a stream of inputs, e.g. bench_one's repeated calls, proj/src/bench.cpp:54-91):
+ * the upload of y runs on its own stream, so it overlaps the downloads of the
+ * previous sweep on this context; up to two sweeps are in flight.  y, xs,
+ * budgets and zero_columns must stay valid until mp_context_wait(ctx, *ticket)
+ * returns, which reports the sweep's status.  mp_bilevel_sweep_host is this
+ * call followed by the wait. */
+mp_status mp_bilevel_sweep_host_async(mp_context* ctx, const void* y, void* const* xs, mp_dtype dtype,
+                                      int64_t n, int64_t m, mp_norm p, mp_norm q, const double* etas,
+                                      int count, double* budgets, int64_t* zero_columns, unsigned flags,
+                                      uint64_t* ticket);
+
+mp_status mp_context_wait(mp_context* ctx, uint64_t ticket);
+
 mp_status mp_multilevel_project_host(mp_context* ctx, const void* t, void* x, mp_dtype dtype,
                                      const int64_t* shape, int order, const mp_norm* levels,
                                      int depth, double eta, double* budget_chain,

@@ -24,7 +24,8 @@ EXPORTS = [
     "mp_project_fibers_workspace_size", "mp_project_fibers",
     "mp_euclid_workspace_size", "mp_euclid_project", "mp_euclid_project_host",
     "mp_context_create", "mp_context_destroy",
-    "mp_bilevel_project_host", "mp_bilevel_sweep_host", "mp_multilevel_project_host",
+    "mp_bilevel_project_host", "mp_bilevel_sweep_host", "mp_bilevel_sweep_host_async", "mp_context_wait",
+    "mp_multilevel_project_host",
     "mp_project_ball_host", "mp_aggregate_host", "mp_perturb_gaussian",
     "mp_profile_events", "mp_profile_timeline", "mp_last_error", "mp_version",
 ]
@@ -103,6 +104,10 @@ def lib() -> C.CDLL:
     L.mp_bilevel_project_host.restype = st
     L.mp_bilevel_sweep_host.argtypes = [vp, vp, vp, en, i64, i64, en, en, vp, C.c_int, vp, vp, u32]
     L.mp_bilevel_sweep_host.restype = st
+    L.mp_bilevel_sweep_host_async.argtypes = [vp, vp, vp, en, i64, i64, en, en, vp, C.c_int, vp, vp, u32, vp]
+    L.mp_bilevel_sweep_host_async.restype = st
+    L.mp_context_wait.argtypes = [vp, C.c_uint64]
+    L.mp_context_wait.restype = st
     L.mp_multilevel_project_host.argtypes = [vp, vp, vp, en, vp, C.c_int, vp, C.c_int, dbl, vp, u32]
     L.mp_multilevel_project_host.restype = st
     L.mp_project_ball_host.argtypes = [vp, vp, vp, en, i64, en, dbl]

@@ -8,7 +8,9 @@
 // proj/src/parallel.cpp:49-58; ours is).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -17,13 +19,37 @@
 
 using namespace mpi;
 
+// One in-flight radius sweep (mp_bilevel_sweep_host_async): its own device
+// copy of Y, two ping-pong outputs, per-radius budgets / info, and a pinned
+// host staging copy of those.
+struct SweepSlot {
+  void* y = nullptr;
+  size_t y_cap = 0;
+  void* out[2] = {nullptr, nullptr};
+  size_t out_cap[2] = {0, 0};
+  void* small = nullptr;  // device: per radius [budgets (m f64) | mp_info]
+  size_t small_cap = 0;
+  void* h_small = nullptr;  // pinned host mirror of small
+  size_t h_small_cap = 0;
+  cudaEvent_t up_done = nullptr, y_free = nullptr, small_done = nullptr, done = nullptr;
+  cudaEvent_t proj_done[2] = {nullptr, nullptr}, dl_done[2] = {nullptr, nullptr};
+  bool used = false;      // the events above have been recorded at least once
+  bool pending = false;   // results not yet collected by mp_context_wait
+  uint64_t ticket = 0;
+  int count = 0;
+  int64_t m = 0;
+  size_t per = 0;
+  double* budgets = nullptr;       // caller's host outputs, filled at wait
+  int64_t* zero_columns = nullptr;
+};
+
 struct mp_context {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // D2H of sweep results (overlaps the next projection)
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  void* out2 = nullptr;  // second output buffer for the sweep ping-pong
-  size_t out2_cap = 0;
+  cudaStream_t up_stream = nullptr;    // H2D of the next sweep's input (overlaps this sweep's D2H)
+  SweepSlot slot[2];
+  uint64_t next_ticket = 1;
   std::mutex mu;
   void* data = nullptr;  // tensor buffer (projected in place)
   size_t data_cap = 0;
@@ -81,12 +107,16 @@ mp_context* mp_context_create(int device) {
   c->device = device;
   DeviceGuard g(device);
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->up_stream, cudaStreamNonBlocking) != cudaSuccess) {
     set_error("mp_context_create: cannot create streams on device %d", device);
     delete c;
     return nullptr;
   }
-  for (auto& e : c->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  for (SweepSlot& sl : c->slot)
+    for (cudaEvent_t* e : {&sl.up_done, &sl.y_free, &sl.small_done, &sl.done, &sl.proj_done[0], &sl.proj_done[1],
+                           &sl.dl_done[0], &sl.dl_done[1]})
+      cudaEventCreateWithFlags(e, cudaEventDisableTiming);
   return c;
 }
 
@@ -98,11 +128,18 @@ void mp_context_destroy(mp_context* c) {
     if (c->data) cudaFree(c->data);
     if (c->ws) cudaFree(c->ws);
     if (c->small) cudaFree(c->small);
-    if (c->out2) cudaFree(c->out2);
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
-    for (auto& e : c->ev)
-      if (e) cudaEventDestroy(e);
+    if (c->up_stream) cudaStreamSynchronize(c->up_stream);
+    for (SweepSlot& sl : c->slot) {
+      for (void* p : {sl.y, sl.out[0], sl.out[1], sl.small})
+        if (p) cudaFree(p);
+      if (sl.h_small) cudaFreeHost(sl.h_small);
+      for (cudaEvent_t e : {sl.up_done, sl.y_free, sl.small_done, sl.done, sl.proj_done[0], sl.proj_done[1],
+                            sl.dl_done[0], sl.dl_done[1]})
+        if (e) cudaEventDestroy(e);
+    }
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->up_stream) cudaStreamDestroy(c->up_stream);
     if (c->stream) cudaStreamDestroy(c->stream);
   }
   delete c;
@@ -180,66 +217,122 @@ mp_status mp_euclid_project_host(mp_context* ctx, const void* y, void* x, mp_dty
   return MP_OK;
 }
 
+namespace {
+
+// Collect a finished sweep: wait for its downloads, check every projection's
+// device status, copy budgets / zero counts to the caller.  Caller holds mu.
+mp_status collect(mp_context* ctx, SweepSlot& sl) {
+  DeviceGuard g(ctx->device);
+  sl.pending = false;
+  MP_CUDA_TRY(cudaEventSynchronize(sl.small_done));
+  MP_CUDA_TRY(cudaEventSynchronize(sl.done));
+  for (int k = 0; k < sl.count; ++k) {
+    const char* hs = static_cast<const char*>(sl.h_small) + sl.per * k;
+    mp_info info;
+    std::memcpy(&info, hs + static_cast<size_t>(sl.m) * sizeof(double), sizeof info);
+    const mp_status st = device_status(info);
+    if (st != MP_OK) return st;
+    if (sl.zero_columns) sl.zero_columns[k] = info.zero_columns;
+    if (sl.budgets) std::memcpy(sl.budgets + static_cast<size_t>(k) * sl.m, hs, static_cast<size_t>(sl.m) * sizeof(double));
+  }
+  return MP_OK;
+}
+
+}  // namespace
+
+mp_status mp_bilevel_sweep_host_async(mp_context* ctx, const void* y, void* const* xs, mp_dtype dtype, int64_t n,
+                                      int64_t m, mp_norm p, mp_norm q, const double* etas, int count, double* budgets,
+                                      int64_t* zero_columns, unsigned flags, uint64_t* ticket) {
+  if (!ctx) ctx = default_ctx();
+  if (!ctx) return fail(MP_ERR_CUDA, "no CUDA context");
+  if (count < 0 || (count > 0 && (!etas || !xs))) return fail(MP_ERR_CONFIG, "bad sweep arguments");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g(ctx->device);
+  const size_t ws = mp_bilevel_workspace_size(dtype, n, m, p, q);
+  if (ws == 0)
+    return mp_bilevel_project(y, count > 0 ? xs[0] : nullptr, dtype, n, m, p, q, count > 0 ? etas[0] : 0.0, nullptr,
+                              nullptr, nullptr, flags, nullptr, 0, nullptr);
+  for (int k = 0; k < count; ++k)
+    if (!(etas[k] >= 0.0) || !std::isfinite(etas[k]))
+      return fail(MP_ERR_VALUE, "radius must be a finite nonnegative real");
+  if (!y) return fail(MP_ERR_WORKSPACE, "null tensor pointer");
+  const uint64_t tk = ctx->next_ticket++;
+  SweepSlot& sl = ctx->slot[tk & 1];
+  if (sl.pending) {  // two sweeps in flight at most: the caller skipped a wait
+    const mp_status st = collect(ctx, sl);
+    if (st != MP_OK) return st;
+  }
+  const size_t bytes = static_cast<size_t>(n) * static_cast<size_t>(m) * dtype_size(dtype);
+  const size_t per = ((static_cast<size_t>(m) * sizeof(double) + sizeof(mp_info) + 255) / 256) * 256;
+  if (sl.used) MP_CUDA_TRY(cudaEventSynchronize(sl.done));  // before any buffer of this slot is regrown
+  MP_CUDA_TRY(grow(sl.y, sl.y_cap, bytes));
+  MP_CUDA_TRY(grow(sl.out[0], sl.out_cap[0], bytes));
+  MP_CUDA_TRY(grow(sl.out[1], sl.out_cap[1], bytes));
+  MP_CUDA_TRY(grow(sl.small, sl.small_cap, per * static_cast<size_t>(std::max(count, 1))));
+  MP_CUDA_TRY(grow(ctx->ws, ctx->ws_cap, ws));
+  if (sl.h_small_cap < per * static_cast<size_t>(std::max(count, 1))) {
+    if (sl.h_small) cudaFreeHost(sl.h_small);
+    sl.h_small = nullptr;
+    sl.h_small_cap = 0;
+    MP_CUDA_TRY(cudaMallocHost(&sl.h_small, per * static_cast<size_t>(std::max(count, 1))));
+    sl.h_small_cap = per * static_cast<size_t>(std::max(count, 1));
+  }
+  cudaStream_t s = ctx->stream, cs = ctx->copy_stream, us = ctx->up_stream;
+  // upload on its own stream, once this slot's previous projections are done
+  // with Y -- so it overlaps the other slot's downloads
+  if (sl.used) MP_CUDA_TRY(cudaStreamWaitEvent(us, sl.y_free, 0));
+  MP_CUDA_TRY(cudaMemcpyAsync(sl.y, y, bytes, cudaMemcpyHostToDevice, us));
+  MP_CUDA_TRY(cudaEventRecord(sl.up_done, us));
+  MP_CUDA_TRY(cudaStreamWaitEvent(s, sl.up_done, 0));
+  for (int k = 0; k < count; ++k) {
+    const int b = k & 1;
+    char* sm = static_cast<char*>(sl.small) + per * k;
+    if (k >= 2 || sl.used) MP_CUDA_TRY(cudaStreamWaitEvent(s, sl.dl_done[b], 0));  // buffer b downloaded
+    const mp_status st = mp_bilevel_project(sl.y, sl.out[b], dtype, n, m, p, q, etas[k], reinterpret_cast<double*>(sm),
+                                            nullptr, reinterpret_cast<mp_info*>(sm + static_cast<size_t>(m) * sizeof(double)),
+                                            flags, ctx->ws, ctx->ws_cap, s);
+    if (st != MP_OK) return st;
+    MP_CUDA_TRY(cudaEventRecord(sl.proj_done[b], s));
+    MP_CUDA_TRY(cudaStreamWaitEvent(cs, sl.proj_done[b], 0));
+    MP_CUDA_TRY(cudaMemcpyAsync(xs[k], sl.out[b], bytes, cudaMemcpyDeviceToHost, cs));
+    MP_CUDA_TRY(cudaEventRecord(sl.dl_done[b], cs));
+  }
+  MP_CUDA_TRY(cudaEventRecord(sl.y_free, s));
+  if (count > 0)
+    MP_CUDA_TRY(cudaMemcpyAsync(sl.h_small, sl.small, per * static_cast<size_t>(count), cudaMemcpyDeviceToHost, s));
+  MP_CUDA_TRY(cudaEventRecord(sl.small_done, s));
+  MP_CUDA_TRY(cudaEventRecord(sl.done, cs));
+  sl.used = true;
+  sl.pending = true;
+  sl.ticket = tk;
+  sl.count = count;
+  sl.m = m;
+  sl.per = per;
+  sl.budgets = budgets;
+  sl.zero_columns = zero_columns;
+  if (ticket) *ticket = tk;
+  return MP_OK;
+}
+
+mp_status mp_context_wait(mp_context* ctx, uint64_t ticket) {
+  if (!ctx) ctx = default_ctx();
+  if (!ctx) return fail(MP_ERR_CUDA, "no CUDA context");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  for (SweepSlot& sl : ctx->slot)
+    if (sl.pending && sl.ticket == ticket) return collect(ctx, sl);
+  return MP_OK;  // already collected (or never issued)
+}
+
 mp_status mp_bilevel_sweep_host(mp_context* ctx, const void* y, void* const* xs, mp_dtype dtype, int64_t n, int64_t m,
                                 mp_norm p, mp_norm q, const double* etas, int count, double* budgets,
                                 int64_t* zero_columns, unsigned flags) {
   if (!ctx) ctx = default_ctx();
   if (!ctx) return fail(MP_ERR_CUDA, "no CUDA context");
-  if (count < 0 || (count > 0 && (!etas || !xs))) return fail(MP_ERR_CONFIG, "bad sweep arguments");
-  if (count == 0) return MP_OK;
-  std::lock_guard<std::mutex> lk(ctx->mu);
-  DeviceGuard g(ctx->device);
-  const size_t ws = mp_bilevel_workspace_size(dtype, n, m, p, q);
-  if (ws == 0)
-    return mp_bilevel_project(y, xs[0], dtype, n, m, p, q, etas[0], nullptr, nullptr, nullptr, flags, nullptr, 0,
-                              nullptr);
-  for (int k = 0; k < count; ++k)
-    if (!(etas[k] >= 0.0) || !std::isfinite(etas[k]))
-      return fail(MP_ERR_VALUE, "radius must be a finite nonnegative real");
-  if (!y) return fail(MP_ERR_WORKSPACE, "null tensor pointer");
-  const size_t bytes = static_cast<size_t>(n) * static_cast<size_t>(m) * dtype_size(dtype);
-  const size_t per = ((static_cast<size_t>(m) * sizeof(double) + sizeof(mp_info) + 255) / 256) * 256;
-  MP_CUDA_TRY(grow(ctx->data, ctx->data_cap, 2 * ((bytes + 255) / 256) * 256));  // y + out[0]
-  MP_CUDA_TRY(grow(ctx->out2, ctx->out2_cap, bytes));                           // out[1]
-  MP_CUDA_TRY(grow(ctx->ws, ctx->ws_cap, ws));
-  MP_CUDA_TRY(grow(ctx->small, ctx->small_cap, per * static_cast<size_t>(count)));
-  char* dy = static_cast<char*>(ctx->data);
-  void* dout[2] = {dy + ((bytes + 255) / 256) * 256, ctx->out2};
-  cudaStream_t s = ctx->stream, cs = ctx->copy_stream;
-  // One upload; each projection writes a ping-pong buffer whose download on
-  // the copy stream overlaps the next projection (the reference's radius
-  // sweep, proj/src/bench.cpp:93-106, re-uploads nothing either).
-  MP_CUDA_TRY(cudaMemcpyAsync(dy, y, bytes, cudaMemcpyHostToDevice, s));
-  for (int k = 0; k < count; ++k) {
-    const int b = k & 1;
-    char* sm = static_cast<char*>(ctx->small) + per * k;
-    if (k >= 2) MP_CUDA_TRY(cudaStreamWaitEvent(s, ctx->ev[2 + b], 0));  // buffer b downloaded
-    mp_status st = mp_bilevel_project(dy, dout[b], dtype, n, m, p, q, etas[k], reinterpret_cast<double*>(sm), nullptr,
-                                      reinterpret_cast<mp_info*>(sm + static_cast<size_t>(m) * sizeof(double)), flags,
-                                      ctx->ws, ctx->ws_cap, s);
-    if (st != MP_OK) return st;
-    MP_CUDA_TRY(cudaEventRecord(ctx->ev[b], s));
-    MP_CUDA_TRY(cudaStreamWaitEvent(cs, ctx->ev[b], 0));
-    MP_CUDA_TRY(cudaMemcpyAsync(xs[k], dout[b], bytes, cudaMemcpyDeviceToHost, cs));
-    MP_CUDA_TRY(cudaEventRecord(ctx->ev[2 + b], cs));
-  }
-  std::vector<mp_info> infos(static_cast<size_t>(count));
-  for (int k = 0; k < count; ++k) {
-    char* sm = static_cast<char*>(ctx->small) + per * k;
-    MP_CUDA_TRY(cudaMemcpyAsync(&infos[k], sm + static_cast<size_t>(m) * sizeof(double), sizeof(mp_info),
-                                cudaMemcpyDeviceToHost, s));
-    if (budgets)
-      MP_CUDA_TRY(cudaMemcpyAsync(budgets + static_cast<size_t>(k) * m, sm, static_cast<size_t>(m) * sizeof(double),
-                                  cudaMemcpyDeviceToHost, s));
-  }
-  MP_CUDA_TRY(cudaStreamSynchronize(s));
-  MP_CUDA_TRY(cudaStreamSynchronize(cs));
-  for (int k = 0; k < count; ++k) {
-    mp_status st = device_status(infos[k]);
-    if (st != MP_OK) return st;
-    if (zero_columns) zero_columns[k] = infos[k].zero_columns;
-  }
-  return MP_OK;
+  uint64_t tk = 0;
+  const mp_status st =
+      mp_bilevel_sweep_host_async(ctx, y, xs, dtype, n, m, p, q, etas, count, budgets, zero_columns, flags, &tk);
+  if (st != MP_OK || tk == 0) return st;
+  return mp_context_wait(ctx, tk);
 }
 
 mp_status mp_multilevel_project_host(mp_context* ctx, const void* t, void* x, mp_dtype dtype, const int64_t* shape,

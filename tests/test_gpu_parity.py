@@ -408,3 +408,38 @@ def test_beyond_int32_element_count(q):
         np.testing.assert_allclose(xc, ref, rtol=1e-6, atol=1e-7)
     del y, x
     torch.cuda.empty_cache()
+
+
+def test_async_sweeps_pipeline_equals_synchronous():
+    """mp_bilevel_sweep_host_async: several sweeps in flight on one context
+    (including a third issued without a wait) give the synchronous results."""
+    import ctypes as C
+    from paper_2405_02086_b200 import _capi
+    lib = _capi.lib()
+    rng = np.random.default_rng(9)
+    n, m = 300, 700
+    ys = [rng.normal(size=(n, m)).astype(np.float32) for _ in range(4)]
+    etas = np.ascontiguousarray([0.01, 0.2, 0.6], np.float64) * float(np.abs(ys[0]).max(axis=0).sum())
+    ref = [mp.bilevel_radius_sweep(y, etas) for y in ys]
+    ctx = lib.mp_context_create(0)
+    outs = [[np.empty_like(ys[0]) for _ in etas] for _ in ys]
+    zeros = [np.empty(len(etas), np.int64) for _ in ys]
+    buds = [np.empty((len(etas), m)) for _ in ys]
+    tks = []
+    for i, y in enumerate(ys):
+        ptrs = (C.c_void_p * len(etas))(*[C.c_void_p(o.ctypes.data) for o in outs[i]])
+        tk = C.c_uint64()
+        _capi.check(lib.mp_bilevel_sweep_host_async(ctx, y.ctypes.data, ptrs, _capi.MP_F32, n, m, 0, 2,
+                                                    etas.ctypes.data, len(etas), buds[i].ctypes.data,
+                                                    zeros[i].ctypes.data, 0, C.byref(tk)))
+        tks.append(tk.value)
+        if i == 1:
+            _capi.check(lib.mp_context_wait(ctx, tks[0]))
+    for tk in tks:
+        _capi.check(lib.mp_context_wait(ctx, tk))
+    lib.mp_context_destroy(ctx)
+    for i in range(len(ys)):
+        for k in range(len(etas)):
+            xr, br, zr = ref[i][k]
+            assert bit_equal(outs[i][k], xr)
+            assert np.array_equal(buds[i][k], np.asarray(br)) and zeros[i][k] == zr
