@@ -28,9 +28,9 @@
 // exact iterate: a thread partial sums <= RPT nonnegative f32 terms, so
 // S >= S_exact (1 - RPT 2^-24) and S_lo = S (1 - 2^-17), rounded down, is
 // below S_exact; t' = RD((S_lo - RU(u_j)) / K) <= (S_exact - u_j) / K.
-// Michelot from below stays below tau and the set only shrinks.  EXACT
-// (near convergence -- the count dropped by < 1/16 -- and always for f64
-// strips): f64 sums, plus min |y| over the set.  With t_ex = (S - u_j) / K,
+// Michelot from below stays below tau and the set only shrinks (f64 strips:
+// f64 sums, the step nudged 2^-45 below).  EXACT (near convergence -- the
+// count dropped by < 1/16): f64 sums, plus min |y| over the set.  With t_ex = (S - u_j) / K,
 // the set is the fixed point {|y| > tau} iff min_set |y| > t_ex, and then
 // tau_j = t_ex: the same fixed point (hence the reference's set
 // {|y| >= cutoff}) that the exact iteration reaches -- one pass before it
@@ -38,6 +38,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <type_traits>
 
 #include "mp_cuda.h"
 #include "mp_kernels.cuh"
@@ -92,9 +94,22 @@ __device__ __forceinline__ FastPart rp_shfl(const FastPart& a, int o) {
   return {__shfl_xor_sync(0xffffffffu, a.s, o), __shfl_xor_sync(0xffffffffu, a.k, o)};
 }
 
+// f64 strips: f64 sum, f32 count.
+struct FastPartD {
+  double s;
+  float k;
+};
+__device__ __forceinline__ FastPartD rp_add(const FastPartD& a, const FastPartD& b) { return {a.s + b.s, a.k + b.k}; }
+__device__ __forceinline__ FastPartD rp_shfl(const FastPartD& a, int o) {
+  return {__shfl_xor_sync(0xffffffffu, a.s, o), __shfl_xor_sync(0xffffffffu, a.k, o)};
+}
+
 // Field-wise select (a ternary on the aggregates would index the array with a
 // runtime value and send it to local memory).
 __device__ __forceinline__ FastPart rp_sel(bool p, const FastPart& a, const FastPart& b) {
+  return {p ? a.s : b.s, p ? a.k : b.k};
+}
+__device__ __forceinline__ FastPartD rp_sel(bool p, const FastPartD& a, const FastPartD& b) {
   return {p ? a.s : b.s, p ? a.k : b.k};
 }
 template <typename T>
@@ -174,7 +189,9 @@ __global__ void __launch_bounds__(kRegThreads, 1)
   tl_begin(3);
   if (info->status != MP_OK) return;
 
-  __shared__ FastPart wf[2][NW][W];
+  using FP = std::conditional_t<kF32, FastPart, FastPartD>;  // fast-pass partial
+  using AccT = std::conditional_t<kF32, float, double>;
+  __shared__ FP wf[2][NW][W];
   __shared__ RegPart<T> wx[2][NW][W];
   int npass = 0, nx = 0, nst = 0;
   for (;;) {
@@ -210,21 +227,22 @@ __global__ void __launch_bounds__(kRegThreads, 1)
     const bool any_proj = __any_sync(0xffffffffu, pj);
 
     if (any_proj) {
-      bool xp = !kF32;  // exact pass (CTA-uniform)
+      bool xp = false;  // exact pass (CTA-uniform)
       for (int par = 0, it = 0; it < 4 * 1024; par ^= 1, ++it) {
         ++npass;
         nx += xp;
         if (!xp) {
-          FastPart a[C4];
+          FP a[C4];
 #pragma unroll
           for (int c = 0; c < C4; ++c) {
-            float sf = 0.0f, kf = 0.0f;
-            const float th = (livem >> c) & 1u ? static_cast<float>(thr[c]) : INFINITY;
+            AccT sf = AccT(0);
+            float kf = 0.0f;
+            const T th = (livem >> c) & 1u ? thr[c] : T(INFINITY);
 #pragma unroll
             for (int i = 0; i < RPT; ++i) {
               T e[C4];
               reg_unpack<T>(q[i], e);
-              const float ab = fabsf(static_cast<float>(e[c]));
+              const T ab = kF32 ? fabsf(e[c]) : fabs(e[c]);
               if (ab > th) {
                 sf += ab;
                 kf += 1.0f;
@@ -232,7 +250,7 @@ __global__ void __launch_bounds__(kRegThreads, 1)
             }
             a[c] = {sf, kf};
           }
-          const FastPart wr = reg_reduce<C4, P>(a, lane);
+          const FP wr = reg_reduce<C4, P>(a, lane);
           if (reg_writer<T, P>(lane)) wf[par][warp][reg_col<T, P>(lane)] = wr;
         } else {
           RegPart<T> a[C4];
@@ -267,10 +285,11 @@ __global__ void __launch_bounds__(kRegThreads, 1)
 #pragma unroll
             for (int w = 1; w < NW; ++w) tot = rp_add(tot, wx[par][w][lane]);
           } else {
-            float s32 = 0.0f, k32 = 0.0f;  // <= RPT + 5 + NW f32 terms per sum
+            AccT s32 = AccT(0);  // f32: <= RPT + 5 + NW f32 terms per sum
+            float k32 = 0.0f;
 #pragma unroll
             for (int w = 0; w < NW; ++w) {
-              const FastPart f = wf[par][w][lane];
+              const FP f = wf[par][w][lane];
               s32 += f.s;
               k32 += f.k;
             }
@@ -288,11 +307,16 @@ __global__ void __launch_bounds__(kRegThreads, 1)
               kp = tot.k;
             }
           } else {
-            // a rigorous lower bound of (S_exact - u_j) / K: the f32 sums
-            // carry < 40 * 2^-24 relative error, the margin is 2^-17
-            const float xs = __fsub_rd(__fmul_rd(__double2float_rd(tot.s), 1.0f - 0x1p-17f), uup);
-            const float tn = xs > 0.0f ? __fmul_rd(xs, __frcp_rd(static_cast<float>(tot.k))) : 0.0f;
-            td = fmax(td, static_cast<double>(tn));
+            if constexpr (kF32) {
+              // a rigorous lower bound of (S_exact - u_j) / K: the f32 sums
+              // carry < 40 * 2^-24 relative error, the margin is 2^-17
+              const float xs = __fsub_rd(__fmul_rd(__double2float_rd(tot.s), 1.0f - 0x1p-17f), uup);
+              const float tn = xs > 0.0f ? __fmul_rd(xs, __frcp_rd(static_cast<float>(tot.k))) : 0.0f;
+              td = fmax(td, static_cast<double>(tn));
+            } else {
+              // f64 sums of f64 data: the Michelot step, nudged below rounding
+              td = fmax(td, (tot.s * (1.0 - 0x1p-45) - ul) / static_cast<double>(tot.k));
+            }
             if ((kp - tot.k) * 16 <= tot.k) ex = true;  // near convergence: exact steps from here
             kp = tot.k;
           }
