@@ -3,8 +3,9 @@
 // project_l1_fast_inplace, proj/src/vector_balls.cpp:150-161) with the
 // strip held ENTIRELY IN REGISTERS.
 //
-// One 512-thread CTA owns a strip of W = 4P f32 (2P f64) adjacent columns
-// over all n <= 8192/P rows; thread t holds 16-byte piece t % P of rows
+// One CTA of NT = 512 threads (128 / 256 for short columns, several CTAs per
+// SM) owns a strip of W = 4P f32 (2P f64) adjacent columns over all
+// n <= NT/P * 16 rows; thread t holds 16-byte piece t % P of rows
 // t / P + (512/P) i, i < 16 (64 registers of data, the whole register file
 // of the SM for P = 2, n = 4096).  A warp instruction then touches 32/P rows
 // of 16P bytes (P = 2: whole 32-byte sectors) instead of 32 lines for 16
@@ -159,14 +160,13 @@ __device__ __forceinline__ uint4 reg_pack(const T (&e)[16 / sizeof(T)]) {
   }
 }
 
-template <typename T, int P, bool DERIVE, bool PERSIST>
-__global__ void __launch_bounds__(kRegThreads, 1)
+template <typename T, int P, bool DERIVE, bool PERSIST, int NT = kRegThreads>
+__global__ void __launch_bounds__(NT, kRegThreads / NT)
     k_l1reg(const T* __restrict__ y, T* __restrict__ x, int n, int64_t m, const double* __restrict__ v,
             const double* __restrict__ u, double* __restrict__ tau_out, const mp_info* __restrict__ info,
             const OuterParams* __restrict__ params, double* __restrict__ u_out, int64_t nstrips) {
   constexpr int C4 = 16 / sizeof(T);
   constexpr int W = C4 * P;  // strip columns
-  constexpr int NT = kRegThreads;
   constexpr int NW = NT / 32;
   constexpr int SL = NT / P;  // row slots
   constexpr int RPT = kRegRPT;
@@ -387,16 +387,25 @@ __global__ void __launch_bounds__(kRegThreads, 1)
   tl_end(3);
 }
 
-// Pieces per row for the register path: the widest P whose 8192/P rows hold
-// the column and that divides the columns; 0 when the path does not apply.
+// Geometry of the register path: the widest P whose 8192/P rows hold the
+// column and that divides the columns, and the smallest CTA (128, 256 or 512
+// threads) whose NT/P row slots x 16 hold n -- short columns get small CTAs,
+// several per SM, so one CTA's per-pass barrier and reduction overlap another
+// CTA's pass (256 x 65536: 207 -> 57 us).  P = 0 when the path does not apply.
+struct RegGeom {
+  int P = 0, NT = 0;
+};
 template <typename T>
-inline int l1reg_pieces(int64_t n, int64_t m, int cap) {
+inline RegGeom l1reg_geometry(int64_t n, int64_t m, int cap) {
   constexpr int C4 = 16 / sizeof(T);
   for (int P = 8; P >= 1; P >>= 1) {
     if (cap > 0 && P > cap) continue;
-    if (n <= static_cast<int64_t>(kRegThreads / P) * kRegRPT && m % (C4 * P) == 0) return P;
+    if (n <= static_cast<int64_t>(kRegThreads / P) * kRegRPT && m % (C4 * P) == 0) {
+      for (int nt = 128; nt <= kRegThreads; nt *= 2)
+        if (n <= static_cast<int64_t>(nt / P) * kRegRPT) return {P, nt};
+    }
   }
-  return 0;
+  return {};
 }
 
 }  // namespace mpk

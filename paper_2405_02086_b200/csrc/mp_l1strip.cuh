@@ -209,15 +209,6 @@ inline bool l1reg_disabled() {
   return d;
 }
 
-// MP_L1REG_PERSIST=0: one CTA per strip instead of grid-stride (tuning aid).
-inline bool l1reg_persist() {
-  static const bool d = [] {
-    const char* e = std::getenv("MP_L1REG_PERSIST");
-    return !(e && std::strcmp(e, "0") == 0);
-  }();
-  return d;
-}
-
 // MP_L1REG_P=1|2|4|8 caps the register path's pieces per row (tuning aid).
 inline int l1reg_prefer_p() {
   static const int p = [] {
@@ -227,36 +218,35 @@ inline int l1reg_prefer_p() {
   return p;
 }
 
-template <typename T, int P>
+// Grid-stride CTAs, as many as are co-resident (kRegThreads / NT per SM).
+template <typename T, int P, int NT>
 cudaError_t launch_reg(const T* y, T* x, int64_t n, int64_t m, const double* v, const double* u,
                        const L1StripWs& ws, const mp_info* info, const L1Derive& dv, cudaStream_t s) {
   constexpr int W = 16 / sizeof(T) * P;
+  const int64_t nstrips = m / W;
   cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(kRegThreads);
-  cfg.gridDim = dim3(static_cast<unsigned>(m / W));
+  cfg.blockDim = dim3(NT);
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(nstrips, static_cast<int64_t>(mpi::sm_count()) *
+                                                                           (kRegThreads / NT))));
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  const int64_t nstrips = m / W;
-  if (l1reg_persist()) {
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(nstrips, sms)));
-    if (dv.params)
-      return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, true, true>, y, x, static_cast<int>(n), m, v, u, ws.tau, info,
-                                dv.params, dv.u_out, nstrips);
-    return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, false, true>, y, x, static_cast<int>(n), m, v, u, ws.tau, info,
-                              dv.params, dv.u_out, nstrips);
-  }
   if (dv.params)
-    return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, true, false>, y, x, static_cast<int>(n), m, v, u, ws.tau, info,
+    return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, true, true, NT>, y, x, static_cast<int>(n), m, v, u, ws.tau, info,
                               dv.params, dv.u_out, nstrips);
-  return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, false, false>, y, x, static_cast<int>(n), m, v, u, ws.tau, info,
+  return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, false, true, NT>, y, x, static_cast<int>(n), m, v, u, ws.tau, info,
                             dv.params, dv.u_out, nstrips);
+}
+
+template <typename T, int P>
+cudaError_t launch_reg_nt(int nt, const T* y, T* x, int64_t n, int64_t m, const double* v, const double* u,
+                          const L1StripWs& ws, const mp_info* info, const L1Derive& dv, cudaStream_t s) {
+  if (nt == 128) return launch_reg<T, P, 128>(y, x, n, m, v, u, ws, info, dv, s);
+  if (nt == 256) return launch_reg<T, P, 256>(y, x, n, m, v, u, ws, info, dv, s);
+  return launch_reg<T, P, kRegThreads>(y, x, n, m, v, u, ws, info, dv, s);
 }
 
 template <typename T>
@@ -313,11 +303,12 @@ cudaError_t launch_l1strip(const T* y, T* x, int64_t n, int64_t m, const double*
                            const L1StripWs& ws, const mp_info* info, unsigned flags, cudaStream_t s,
                            const L1Derive& dv = L1Derive()) {
   if (l1_quad_ok<T>(y, x, m) && !l1reg_disabled()) {
-    switch (l1reg_pieces<T>(n, m, l1reg_prefer_p())) {
-      case 8: return launch_reg<T, 8>(y, x, n, m, v, u, ws, info, dv, s);
-      case 4: return launch_reg<T, 4>(y, x, n, m, v, u, ws, info, dv, s);
-      case 2: return launch_reg<T, 2>(y, x, n, m, v, u, ws, info, dv, s);
-      case 1: return launch_reg<T, 1>(y, x, n, m, v, u, ws, info, dv, s);
+    const RegGeom g = l1reg_geometry<T>(n, m, l1reg_prefer_p());
+    switch (g.P) {
+      case 8: return launch_reg_nt<T, 8>(g.NT, y, x, n, m, v, u, ws, info, dv, s);
+      case 4: return launch_reg_nt<T, 4>(g.NT, y, x, n, m, v, u, ws, info, dv, s);
+      case 2: return launch_reg_nt<T, 2>(g.NT, y, x, n, m, v, u, ws, info, dv, s);
+      case 1: return launch_reg_nt<T, 1>(g.NT, y, x, n, m, v, u, ws, info, dv, s);
       default: break;
     }
   }
