@@ -6,7 +6,7 @@
 // One CTA of NT = 512 threads (128 / 256 for short columns, several CTAs per
 // SM) owns a strip of W = 4P f32 (2P f64) adjacent columns over all
 // n <= NT/P * 16 rows; thread t holds 16-byte piece t % P of rows
-// t / P + (512/P) i, i < 16 (64 registers of data, the whole register file
+// t / P + (NT/P) i, i < 16 (64 registers of data, the whole register file
 // of the SM for P = 2, n = 4096).  A warp instruction then touches 32/P rows
 // of 16P bytes (P = 2: whole 32-byte sectors) instead of 32 lines for 16
 // bytes each -- the L1 line rate, not HBM, bounds a 16-byte-per-row walk.
