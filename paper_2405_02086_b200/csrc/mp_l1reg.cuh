@@ -387,24 +387,27 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
   tl_end(3);
 }
 
-// Geometry of the register path: the widest P whose 8192/P rows hold the
-// column and that divides the columns, and the smallest CTA (128, 256 or 512
-// threads) whose NT/P row slots x 16 hold n -- short columns get small CTAs,
-// several per SM, so one CTA's per-pass barrier and reduction overlap another
-// CTA's pass (256 x 65536: 207 -> 57 us).  P = 0 when the path does not apply.
+// Geometry of the register path: the smallest CTA (128, 256 or 512 threads)
+// whose NT/P row slots x 16 hold n with P >= 2, and within it the widest P
+// that divides the columns; P = 1 (16-byte rows, L1-line-rate bound) only
+// when nothing else fits.  Several small CTAs per SM overlap one CTA's
+// per-pass barrier and reduction with another's pass, which beats wider rows
+// (K3b: 256x65536 207 -> 57 us; 1000x16384 74 -> 56; 2000x32768 240 -> 211).
+// P = 0 when the path does not apply.
 struct RegGeom {
   int P = 0, NT = 0;
 };
 template <typename T>
 inline RegGeom l1reg_geometry(int64_t n, int64_t m, int cap) {
   constexpr int C4 = 16 / sizeof(T);
-  for (int P = 8; P >= 1; P >>= 1) {
-    if (cap > 0 && P > cap) continue;
-    if (n <= static_cast<int64_t>(kRegThreads / P) * kRegRPT && m % (C4 * P) == 0) {
-      for (int nt = 128; nt <= kRegThreads; nt *= 2)
-        if (n <= static_cast<int64_t>(nt / P) * kRegRPT) return {P, nt};
-    }
-  }
+  auto fits = [&](int P, int nt) {
+    return (cap <= 0 || P <= cap) && n <= static_cast<int64_t>(nt / P) * kRegRPT && m % (C4 * P) == 0;
+  };
+  for (int nt = 128; nt <= kRegThreads; nt *= 2)
+    for (int P = 8; P >= 2; P >>= 1)
+      if (fits(P, nt)) return {P, nt};
+  for (int nt = 128; nt <= kRegThreads; nt *= 2)
+    if (fits(1, nt)) return {1, nt};
   return {};
 }
 
