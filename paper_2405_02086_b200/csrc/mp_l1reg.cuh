@@ -160,7 +160,7 @@ __device__ __forceinline__ uint4 reg_pack(const T (&e)[16 / sizeof(T)]) {
   }
 }
 
-template <typename T, int P, bool DERIVE, bool PERSIST, int NT = kRegThreads>
+template <typename T, int P, bool DERIVE, bool PERSIST, int NT = kRegThreads, int RS = 0>
 __global__ void __launch_bounds__(NT, kRegThreads / NT)
     k_l1reg(const T* __restrict__ y, T* __restrict__ x, int n, int64_t m, const double* __restrict__ v,
             const double* __restrict__ u, double* __restrict__ tau_out, const mp_info* __restrict__ info,
@@ -177,6 +177,22 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
   const int rb = tid / P;         // this thread's first row
   const int64_t step = static_cast<int64_t>(SL) * m;
 
+  // RS > 0: the strip's last RS pieces per thread live in shared memory
+  // ([RS][NT] uint4, each thread lands and reads back only its own), the
+  // first RPT in registers -- half the registers per strip, two CTAs per SM.
+  extern __shared__ __align__(16) uint4 sq[];
+  constexpr int NPC = RPT + RS;  // pieces per thread
+  auto land_smem = [&](int64_t s_strip) {
+    if constexpr (RS > 0) {
+      const T* yp = y + static_cast<int64_t>(rb + SL * RPT) * m + s_strip * W + pc;
+#pragma unroll
+      for (int i = 0; i < RS; ++i, yp += step) {
+        if (rb + SL * (RPT + i) < n) cp_async_16(&sq[i * NT + tid], yp);
+        else sq[i * NT + tid] = make_uint4(0, 0, 0, 0);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+  };
   // Land the first strip: y is not written by K1 / K2.
   uint4 q[RPT];
   {
@@ -185,10 +201,15 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
     for (int i = 0; i < RPT; ++i, yp += step)
       q[i] = rb + SL * i < n ? __ldg(reinterpret_cast<const uint4*>(yp)) : make_uint4(0, 0, 0, 0);
   }
+  land_smem(strip);
   pdl_wait();
   tl_begin(3);
   if (info->status != MP_OK) return;
 
+  auto piece = [&](int i) -> uint4 {  // i is a compile-time index after unrolling
+    if (RS == 0 || i < RPT) return q[i < RPT ? i : 0];
+    return sq[(i - RPT) * NT + tid];
+  };
   using FP = std::conditional_t<kF32, FastPart, FastPartD>;  // fast-pass partial
   using AccT = std::conditional_t<kF32, float, double>;
   __shared__ FP wf[2][NW][W];
@@ -225,6 +246,7 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
       if (DERIVE && u_out && warp == 0) u_out[strip * W + lane] = ul;
     }
     const bool any_proj = __any_sync(0xffffffffu, pj);
+    if constexpr (RS > 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
 
     if (any_proj) {
       bool xp = false;  // exact pass (CTA-uniform)
@@ -239,9 +261,9 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
             float kf = 0.0f;
             const T th = (livem >> c) & 1u ? thr[c] : T(INFINITY);
 #pragma unroll
-            for (int i = 0; i < RPT; ++i) {
+            for (int i = 0; i < NPC; ++i) {
               T e[C4];
-              reg_unpack<T>(q[i], e);
+              reg_unpack<T>(piece(i), e);
               const T ab = kF32 ? fabsf(e[c]) : fabs(e[c]);
               if (ab > th) {
                 sf += ab;
@@ -261,9 +283,9 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
             T mn = T(INFINITY);
             const T th = (livem >> c) & 1u ? thr[c] : T(INFINITY);
 #pragma unroll
-            for (int i = 0; i < RPT; ++i) {
+            for (int i = 0; i < NPC; ++i) {
               T e[C4];
-              reg_unpack<T>(q[i], e);
+              reg_unpack<T>(piece(i), e);
               const T ab = kF32 ? fabsf(e[c]) : fabs(e[c]);
               if (ab > th) {
                 sd += static_cast<double>(ab);
@@ -352,11 +374,11 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
     T* xq = x + static_cast<int64_t>(rb) * m + cb;
     const T* yn = y + static_cast<int64_t>(rb) * m + next * W + pc;
 #pragma unroll
-    for (int i = 0; i < RPT; ++i, xq += step, yn += step) {
+    for (int i = 0; i < NPC; ++i, xq += step, yn += step) {
       if (rb + SL * i >= n) break;
       if (need_store) {
         T e[C4];
-        reg_unpack<T>(q[i], e);
+        reg_unpack<T>(piece(i), e);
 #pragma unroll
         for (int c = 0; c < C4; ++c) {
           const unsigned kd = (kinds >> (2 * c)) & 3u;
@@ -373,7 +395,19 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
         }
         __stcs(reinterpret_cast<uint4*>(xq), reg_pack<T>(e));
       }
-      if (more) q[i] = __ldg(reinterpret_cast<const uint4*>(yn));
+      if (more) {
+        if (i < RPT) q[i < RPT ? i : 0] = __ldg(reinterpret_cast<const uint4*>(yn));
+        else if constexpr (RS > 0) cp_async_16(&sq[(i - RPT) * NT + tid], yn);
+      }
+    }
+    if constexpr (RS > 0) {
+      if (more) {
+        // rows past n of the next strip: zero pieces (none when n fills the slots)
+#pragma unroll
+        for (int i = 0; i < RS; ++i)
+          if (rb + SL * (RPT + i) >= n) sq[i * NT + tid] = make_uint4(0, 0, 0, 0);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
     }
     if (!more) break;
     strip = next;
@@ -387,27 +421,35 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
   tl_end(3);
 }
 
-// Geometry of the register path: the smallest CTA (128, 256 or 512 threads)
-// whose NT/P row slots x 16 hold n with P >= 2, and within it the widest P
-// that divides the columns; P = 1 (16-byte rows, L1-line-rate bound) only
-// when nothing else fits.  Several small CTAs per SM overlap one CTA's
-// per-pass barrier and reduction with another's pass, which beats wider rows
-// (K3b: 256x65536 207 -> 57 us; 1000x16384 74 -> 56; 2000x32768 240 -> 211).
-// P = 0 when the path does not apply.
+// Geometry of the register path.  A CTA of NT threads (128 / 256 / 512, so
+// 4 / 2 / 1 CTAs per SM by registers) holds (NT/P) * (16 + RS) rows: 16 row
+// pieces per thread in registers and, for the hybrid strips (RS = 16, P = 2),
+// 16 more in shared memory.  Preference: registers only with >= 2 CTAs per
+// SM (several CTAs per SM overlap one CTA's per-pass barrier and reduction
+// with another's pass), smallest CTA and widest P >= 2 first; then hybrid
+// strips; then one 512-thread CTA per SM; P = 1 (16-byte rows, L1-line-rate
+// bound) only when nothing else fits.  Measured K3b: 256x65536 207 -> 57 us;
+// 1000x16384 74 -> 56; 2000x32768 240 -> 211; 4096x16384 255 -> 206 (hybrid,
+// 2 CTAs per SM); 6000x8192 201 us.  P = 0 when the path does not apply.
+constexpr int kRegHybridRS = 16;
 struct RegGeom {
-  int P = 0, NT = 0;
+  int P = 0, NT = 0, RS = 0;
 };
 template <typename T>
 inline RegGeom l1reg_geometry(int64_t n, int64_t m, int cap) {
   constexpr int C4 = 16 / sizeof(T);
-  auto fits = [&](int P, int nt) {
-    return (cap <= 0 || P <= cap) && n <= static_cast<int64_t>(nt / P) * kRegRPT && m % (C4 * P) == 0;
+  auto fits = [&](int P, int nt, int rs) {
+    return (cap <= 0 || P <= cap) && n <= static_cast<int64_t>(nt / P) * (kRegRPT + rs) && m % (C4 * P) == 0;
   };
-  for (int nt = 128; nt <= kRegThreads; nt *= 2)
+  for (int nt = 128; nt < kRegThreads; nt *= 2)  // registers only, >= 2 CTAs per SM
     for (int P = 8; P >= 2; P >>= 1)
-      if (fits(P, nt)) return {P, nt};
+      if (fits(P, nt, 0)) return {P, nt, 0};
+  for (int nt = 128; nt <= kRegThreads; nt *= 2)  // hybrid before a lone CTA per SM
+    if (fits(2, nt, kRegHybridRS)) return {2, nt, kRegHybridRS};
+  for (int P = 8; P >= 2; P >>= 1)
+    if (fits(P, kRegThreads, 0)) return {P, kRegThreads, 0};
   for (int nt = 128; nt <= kRegThreads; nt *= 2)
-    if (fits(1, nt)) return {1, nt};
+    if (fits(1, nt, 0)) return {1, nt, 0};
   return {};
 }
 

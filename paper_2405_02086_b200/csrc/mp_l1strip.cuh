@@ -219,15 +219,25 @@ inline int l1reg_prefer_p() {
 }
 
 // Grid-stride CTAs, as many as are co-resident (kRegThreads / NT per SM).
-template <typename T, int P, int NT>
+template <typename T, int P, int NT, int RS = 0>
 cudaError_t launch_reg(const T* y, T* x, int64_t n, int64_t m, const double* v, const double* u,
                        const L1StripWs& ws, const mp_info* info, const L1Derive& dv, cudaStream_t s) {
   constexpr int W = 16 / sizeof(T) * P;
   const int64_t nstrips = m / W;
+  const size_t smem = static_cast<size_t>(NT) * RS * 16;
+  if constexpr (RS > 0) {
+    static const cudaError_t a1 = cudaFuncSetAttribute(k_l1reg<T, P, true, true, NT, RS>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static const cudaError_t a2 = cudaFuncSetAttribute(k_l1reg<T, P, false, true, NT, RS>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (a1 != cudaSuccess) return a1;
+    if (a2 != cudaSuccess) return a2;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(NT);
   cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(nstrips, static_cast<int64_t>(mpi::sm_count()) *
                                                                            (kRegThreads / NT))));
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -235,17 +245,24 @@ cudaError_t launch_reg(const T* y, T* x, int64_t n, int64_t m, const double* v, 
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (dv.params)
-    return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, true, true, NT>, y, x, static_cast<int>(n), m, v, u, ws.tau, info,
-                              dv.params, dv.u_out, nstrips);
-  return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, false, true, NT>, y, x, static_cast<int>(n), m, v, u, ws.tau, info,
-                            dv.params, dv.u_out, nstrips);
+    return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, true, true, NT, RS>, y, x, static_cast<int>(n), m, v, u, ws.tau,
+                              info, dv.params, dv.u_out, nstrips);
+  return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, false, true, NT, RS>, y, x, static_cast<int>(n), m, v, u, ws.tau,
+                            info, dv.params, dv.u_out, nstrips);
 }
 
 template <typename T, int P>
-cudaError_t launch_reg_nt(int nt, const T* y, T* x, int64_t n, int64_t m, const double* v, const double* u,
+cudaError_t launch_reg_nt(const RegGeom& g, const T* y, T* x, int64_t n, int64_t m, const double* v, const double* u,
                           const L1StripWs& ws, const mp_info* info, const L1Derive& dv, cudaStream_t s) {
-  if (nt == 128) return launch_reg<T, P, 128>(y, x, n, m, v, u, ws, info, dv, s);
-  if (nt == 256) return launch_reg<T, P, 256>(y, x, n, m, v, u, ws, info, dv, s);
+  if constexpr (P == 2) {
+    if (g.RS > 0) {
+      if (g.NT == 128) return launch_reg<T, 2, 128, kRegHybridRS>(y, x, n, m, v, u, ws, info, dv, s);
+      if (g.NT == 256) return launch_reg<T, 2, 256, kRegHybridRS>(y, x, n, m, v, u, ws, info, dv, s);
+      return launch_reg<T, 2, kRegThreads, kRegHybridRS>(y, x, n, m, v, u, ws, info, dv, s);
+    }
+  }
+  if (g.NT == 128) return launch_reg<T, P, 128>(y, x, n, m, v, u, ws, info, dv, s);
+  if (g.NT == 256) return launch_reg<T, P, 256>(y, x, n, m, v, u, ws, info, dv, s);
   return launch_reg<T, P, kRegThreads>(y, x, n, m, v, u, ws, info, dv, s);
 }
 
@@ -305,10 +322,10 @@ cudaError_t launch_l1strip(const T* y, T* x, int64_t n, int64_t m, const double*
   if (l1_quad_ok<T>(y, x, m) && !l1reg_disabled()) {
     const RegGeom g = l1reg_geometry<T>(n, m, l1reg_prefer_p());
     switch (g.P) {
-      case 8: return launch_reg_nt<T, 8>(g.NT, y, x, n, m, v, u, ws, info, dv, s);
-      case 4: return launch_reg_nt<T, 4>(g.NT, y, x, n, m, v, u, ws, info, dv, s);
-      case 2: return launch_reg_nt<T, 2>(g.NT, y, x, n, m, v, u, ws, info, dv, s);
-      case 1: return launch_reg_nt<T, 1>(g.NT, y, x, n, m, v, u, ws, info, dv, s);
+      case 8: return launch_reg_nt<T, 8>(g, y, x, n, m, v, u, ws, info, dv, s);
+      case 4: return launch_reg_nt<T, 4>(g, y, x, n, m, v, u, ws, info, dv, s);
+      case 2: return launch_reg_nt<T, 2>(g, y, x, n, m, v, u, ws, info, dv, s);
+      case 1: return launch_reg_nt<T, 1>(g, y, x, n, m, v, u, ws, info, dv, s);
       default: break;
     }
   }
