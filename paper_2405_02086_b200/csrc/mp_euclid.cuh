@@ -282,12 +282,16 @@ __global__ void __launch_bounds__(kEuSearchThreads)
     sc->part[0][b].tmax = tmax;
   }
   grid.sync();
+  // CTA partials reduced by every CTA with the same fixed tree (thread i
+  // loads partials i, i + 256, ...), so all CTAs agree bit for bit
   DD L{0.0, 0.0};
   double TM = 0.0;
-  for (int i = 0; i < G; ++i) {  // CTA order, identical in every CTA
+  for (int i = tid; i < G; i += blockDim.x) {
     L = dd_add(L, sc->part[0][i].l1inf);
     TM = fmax(TM, sc->part[0][i].tmax);
   }
+  L = block_sum_dd(L, dscr);
+  TM = -block_min(-TM, fscr);
   const double l1inf = L.hi + L.lo;
   double theta;
   int iters = 0;
@@ -333,13 +337,17 @@ __global__ void __launch_bounds__(kEuSearchThreads)
       B = DD{0.0, 0.0};
       lo = 0.0;
       hi = __longlong_as_double(0x7ff0000000000000ll);
-      for (int i = 0; i < G; ++i) {
+      for (int i = tid; i < G; i += blockDim.x) {
         const EuPart& p = sc->part[par][i];
         A = dd_add(A, p.a);
         B = dd_add(B, p.b);
         lo = fmax(lo, p.lo);
         hi = fmin(hi, p.hi);
       }
+      A = block_sum_dd(A, dscr);
+      B = block_sum_dd(B, dscr);
+      lo = -block_min(-lo, fscr);
+      hi = block_min(hi, fscr);
       const double tn = dd_div_to_double(dd_sub(A, DD{eta, 0.0}), B);
       if (tn <= hi || !(tn > theta)) {  // the root lies on this segment
         theta = fmin(fmax(tn, lo), hi);
