@@ -933,13 +933,15 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   // Zero-budget packs are stored without a read, but only when the whole
-  // 8-lane group (128 contiguous bytes) is zero-budget: a line half written
-  // early by a read-free pack and half late by a loading one is evicted
-  // partially valid and costs a DRAM read-modify-write (f64 l_inf with 37%
-  // zero columns: K3 410 -> 174 us at 4096x16384).  Lanes past m count as dead.
+  // 16-lane group (256 contiguous bytes) is zero-budget: lines written partly
+  // early by read-free packs and partly late by loading ones are evicted
+  // partially valid and cost DRAM read-modify-writes.  Measured group sizes
+  // (f64 l_inf 4096x16384 K3 / config-5 iteration 0 projection, 90% zero
+  // columns): 1 lane 405 us / 1.13 ms, 2: 183 / 0.65, 8: 175 / 0.54,
+  // 16: 174 / 0.53, 32: 176 / 0.53.  Lanes past m count as dead.
   {
     const int lane = threadIdx.x & 31;
-    const unsigned grp = 0xffu << (lane & ~7);
+    const unsigned grp = 0xffffu << (lane & 16);
     const unsigned db = __ballot_sync(__activemask(), dead) | ~__activemask();
     dead = (db & grp) == grp;
   }
