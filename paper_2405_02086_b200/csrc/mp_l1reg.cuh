@@ -253,47 +253,53 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
       for (int par = 0, it = 0; it < 4 * 1024; par ^= 1, ++it) {
         ++npass;
         nx += xp;
+        // Pieces outer, columns inner: each piece (a shared-memory load for the
+        // hybrid part) is read once per pass and feeds C4 independent chains;
+        // every column still sums its pieces in ascending i.
         if (!xp) {
           FP a[C4];
+          T th[C4];
 #pragma unroll
           for (int c = 0; c < C4; ++c) {
-            AccT sf = AccT(0);
-            float kf = 0.0f;
-            const T th = (livem >> c) & 1u ? thr[c] : T(INFINITY);
+            a[c] = {AccT(0), 0.0f};
+            th[c] = (livem >> c) & 1u ? thr[c] : T(INFINITY);
+          }
 #pragma unroll
-            for (int i = 0; i < NPC; ++i) {
-              T e[C4];
-              reg_unpack<T>(piece(i), e);
+          for (int i = 0; i < NPC; ++i) {
+            T e[C4];
+            reg_unpack<T>(piece(i), e);
+#pragma unroll
+            for (int c = 0; c < C4; ++c) {
               const T ab = kF32 ? fabsf(e[c]) : fabs(e[c]);
-              if (ab > th) {
-                sf += ab;
-                kf += 1.0f;
+              if (ab > th[c]) {
+                a[c].s += ab;
+                a[c].k += 1.0f;
               }
             }
-            a[c] = {sf, kf};
           }
           const FP wr = reg_reduce<C4, P>(a, lane);
           if (reg_writer<T, P>(lane)) wf[par][warp][reg_col<T, P>(lane)] = wr;
         } else {
           RegPart<T> a[C4];
+          T th[C4];
 #pragma unroll
           for (int c = 0; c < C4; ++c) {
-            double sd = 0.0;
-            int kk = 0;
-            T mn = T(INFINITY);
-            const T th = (livem >> c) & 1u ? thr[c] : T(INFINITY);
+            a[c] = {0.0, 0, T(INFINITY)};
+            th[c] = (livem >> c) & 1u ? thr[c] : T(INFINITY);
+          }
 #pragma unroll
-            for (int i = 0; i < NPC; ++i) {
-              T e[C4];
-              reg_unpack<T>(piece(i), e);
+          for (int i = 0; i < NPC; ++i) {
+            T e[C4];
+            reg_unpack<T>(piece(i), e);
+#pragma unroll
+            for (int c = 0; c < C4; ++c) {
               const T ab = kF32 ? fabsf(e[c]) : fabs(e[c]);
-              if (ab > th) {
-                sd += static_cast<double>(ab);
-                ++kk;
-                mn = ab < mn ? ab : mn;
+              if (ab > th[c]) {
+                a[c].s += static_cast<double>(ab);
+                ++a[c].k;
+                a[c].mn = ab < a[c].mn ? ab : a[c].mn;
               }
             }
-            a[c] = {sd, kk, mn};
           }
           const RegPart<T> wr = reg_reduce<C4, P>(a, lane);
           if (reg_writer<T, P>(lane)) wx[par][warp][reg_col<T, P>(lane)] = wr;
@@ -363,13 +369,27 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
     // store, so its loads overlap this strip's apply
     const int64_t next = strip + gridDim.x;
     const bool more = PERSIST && next < nstrips;
-    double t[C4];
-    TauPair tp[C4];
+    // One branch-free rule for every column kind: d = (|y| - tau_hi) - tau_lo;
+    // x = d > 0 ? copysign(d, y) : (y & keep).  Feasible columns: tau = 0 and
+    // keep = all ones (d = |y| exactly, zeros keep their sign: x = y);
+    // zero budget: tau = +inf, keep = 0 (+0.0); projected: tau_j, keep = 0
+    // (the soft threshold's +0.0, proj/src/vector_balls.cpp:42-48).
+    using UT = std::conditional_t<kF32, unsigned, unsigned long long>;
+    T th_hi[C4], th_lo[C4];
+    UT keep[C4];
 #pragma unroll
     for (int c = 0; c < C4; ++c) {
-      t[c] = __shfl_sync(0xffffffffu, td, pc + c);
-      tp[c].hi = __double2float_rn(t[c]);
-      tp[c].lo = __double2float_rn(t[c] - static_cast<double>(tp[c].hi));
+      const double tc = __shfl_sync(0xffffffffu, td, pc + c);
+      const unsigned kd = (kinds >> (2 * c)) & 3u;
+      keep[c] = kd == 1u ? ~UT(0) : UT(0);
+      if constexpr (kF32) {
+        const TauPair tq{__double2float_rn(tc), __double2float_rn(tc - static_cast<double>(__double2float_rn(tc)))};
+        th_hi[c] = kd == 1u ? 0.0f : (kd == 2u ? INFINITY : tq.hi);
+        th_lo[c] = kd == 3u ? tq.lo : 0.0f;
+      } else {
+        th_hi[c] = kd == 1u ? 0.0 : (kd == 2u ? static_cast<double>(INFINITY) : tc);
+        th_lo[c] = 0.0;
+      }
     }
     T* xq = x + static_cast<int64_t>(rb) * m + cb;
     const T* yn = y + static_cast<int64_t>(rb) * m + next * W + pc;
@@ -381,16 +401,14 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
         reg_unpack<T>(piece(i), e);
 #pragma unroll
         for (int c = 0; c < C4; ++c) {
-          const unsigned kd = (kinds >> (2 * c)) & 3u;
-          if (kd == 2u) e[c] = T(0);
-          else if (kd == 3u) {
-            if constexpr (kF32) {
-              const float dm = shrink_mag(fabsf(e[c]), tp[c]);
-              e[c] = dm > 0.0f ? copysignf(dm, e[c]) : 0.0f;
-            } else {
-              const double dm = fabs(e[c]) - t[c];
-              e[c] = dm > 0.0 ? copysign(dm, e[c]) : 0.0;
-            }
+          if constexpr (kF32) {
+            const float dm = shrink_mag(fabsf(e[c]), TauPair{th_hi[c], th_lo[c]});
+            e[c] = dm > 0.0f ? copysignf(dm, e[c]) : __uint_as_float(__float_as_uint(e[c]) & keep[c]);
+          } else {
+            const double dm = fabs(e[c]) - th_hi[c];
+            e[c] = dm > 0.0 ? copysign(dm, e[c])
+                            : __longlong_as_double(static_cast<long long>(
+                                  static_cast<UT>(__double_as_longlong(e[c])) & keep[c]));
           }
         }
         __stcs(reinterpret_cast<uint4*>(xq), reg_pack<T>(e));
