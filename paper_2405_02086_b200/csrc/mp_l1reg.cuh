@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
     double ul = 0.0, td = -1.0;
     float uup = 0.0f;  // RU(u_j)
     int kp = n + 1;
-    bool lv = false, ex = !kF32, pj = false;
+    bool lv = false, ex = false, pj = false;
     if (lane < W) {
       const double vj = v[strip * W + lane];
       ul = DERIVE ? derive_u(*params, vj) : u[strip * W + lane];
