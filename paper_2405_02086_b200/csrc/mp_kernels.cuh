@@ -884,8 +884,10 @@ __device__ __forceinline__ double load_norm(const ApplyCols& a, int64_t c) {
 // l_inf clamp (proj/src/fiber_kernels.cpp:43-49) / l2 scale (:50-55).
 // `dead` column groups (u == 0) are written as +0 without a read unless
 // MP_FLAG_EXACT_ZERO_SIGN.
+// f32 l2 runs at 4 CTAs per SM (<= 64 registers): 143.4 vs 145.4 us on config 3
+// l1,2 at the 5 CTAs its 48 registers would allow (a grid of fewer row slots).
 template <typename T, int VEC, int Q, int U, bool DERIVE>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, (Q == kL2 && sizeof(T) == 4) ? 4 : 0)
     k_apply(const T* __restrict__ y, T* __restrict__ x, int64_t n, int64_t m, int64_t rpb, int interleave,
             ApplyCols A, const mp_info* __restrict__ info, unsigned flags) {
   pdl_wait();
@@ -960,6 +962,19 @@ __global__ void __launch_bounds__(kThreads)
     tl_end(3);
     return;
   }
+  // f32 l2 scale: the f64 factor as a float pair (hi + lo), the product
+  // y * factor formed in f32 with an exact FMA error term -- full-rate FP32
+  // instead of two f32<->f64 converts (1/8 rate) and a DMUL per element.
+  // Magnitudes, then the sign: factor 1 and 0 keep y's zero sign (y * 1.0,
+  // y * 0.0 in the reference's doubles).
+  float fh[VEC], fl[VEC];
+  if constexpr (Q == kL2 && sizeof(T) == 4) {
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      fh[j] = __double2float_rn(pu[j]);
+      fl[j] = __double2float_rn(pu[j] - static_cast<double>(fh[j]));
+    }
+  }
   auto op = [&](T e, int j) -> T {
     if constexpr (Q == kInf) {
       // a zero budget inside a live group: copysign keeps y's zero sign,
@@ -967,8 +982,14 @@ __global__ void __launch_bounds__(kThreads)
       if constexpr (sizeof(T) == 4) return fabsf(e) > rd[j] ? copysignf(rn[j], e) : e;
       else return fabs(e) > pu[j] ? copysign(pu[j], e) : e;
     } else {
-      if constexpr (sizeof(T) == 4) return __double2float_rn(__dmul_rn(static_cast<double>(e), pu[j]));
-      else return __dmul_rn(e, pu[j]);
+      if constexpr (sizeof(T) == 4) {
+        const float a = fabsf(e);
+        const float ph = a * fh[j];
+        const float t = fmaf(a, fl[j], fmaf(a, fh[j], -ph));
+        return copysignf(ph + t, e);
+      } else {
+        return __dmul_rn(e, pu[j]);
+      }
     }
   };
   const T* p = y + last;

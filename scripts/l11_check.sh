@@ -6,4 +6,4 @@ for shp in "4096 16384" "1000 16384" "6000 8192" "256 65536"; do
   N=$1 M=$2 Q=1 DIST=normal RELS=0.05 python scripts/timeline.py
 done > gpurun_out/l11_tl_$TAG.log 2>&1
 DT=float64 N=4096 M=16384 Q=1 DIST=normal RELS=0.05 python scripts/timeline.py >> gpurun_out/l11_tl_$TAG.log 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q ${PYTEST_K} > gpurun_out/pytest_$TAG.log 2>&1; echo pytest=$?
+timeout 900 python -m pytest tests -m gpu -x -q ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_$TAG.log 2>&1; echo pytest=$?
