@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <cstdio>
 #include <mutex>
@@ -701,11 +702,15 @@ struct EuclidWs {
   mpk::EuScratch* sc;
 };
 
+int pow2_at_least(int64_t n);
+
+// The sorted columns are P2-strided (mpk::EuLayout).
 EuclidWs carve_euclid(Carve& c, mp_dtype dt, int64_t n, int64_t m) {
   EuclidWs w{};
+  const size_t ld = static_cast<size_t>(std::max(64, pow2_at_least(n)));
   w.info = c.take<mp_info>(1);
-  w.mags = c.take<char>(static_cast<size_t>(n) * m * dtype_size(dt));
-  w.pref = c.take<mpk::DD>(static_cast<size_t>(n) * m);
+  w.mags = c.take<char>(ld * m * dtype_size(dt));
+  w.pref = c.take<mpk::DD>(ld * m);
   w.colmax = c.take<double>(m);
   w.budgets = c.take<double>(m);
   w.colp = c.take<double>(m);
@@ -745,7 +750,7 @@ mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, doubl
   MP_CUDA_TRY(cudaMemsetAsync(inf, 0, sizeof(mp_info), s));
   T* mags = static_cast<T*>(w.mags);
   mpk::k_eu_gather<T><<<dim3(static_cast<unsigned>((m + 31) / 32), static_cast<unsigned>((n + 31) / 32)), dim3(32, 8),
-                        0, s>>>(y, n, m, mags, inf);
+                        0, s>>>(y, n, m, mags, static_cast<int64_t>(std::max(64, pow2_at_least(n))), inf);
   MP_CUDA_TRY(cudaGetLastError());
   // 16 keys per thread (32 beyond 16384): most of the network runs in
   // registers and shuffles; small columns keep one warp
@@ -753,7 +758,23 @@ mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, doubl
   const int ek = P2 >= 512 ? std::max(16, P2 / mpk::kEuSortThreads) : P2 / 32;
   const int nt = P2 / ek;
   const size_t smem = static_cast<size_t>(P2) * sizeof(T);
-  switch (P2 / nt) {
+  // radix-sorted columns (cub::BlockRadixSort, 16 keys per thread) for
+  // 1024 <= P2 <= 16384; MP_EU_SORT=bitonic keeps the network (A/B aid)
+  static const bool bitonic_only = [] {
+    const char* e = std::getenv("MP_EU_SORT");
+    return e && std::strcmp(e, "bitonic") == 0;
+  }();
+  // (the CUB temp storage is static shared memory: <= 48 KiB -> f32 up to
+  // 512 threads, f64 up to 256)
+  constexpr int kRadixMaxNt = sizeof(T) == 4 ? 512 : 256;
+  if (!bitonic_only && ek == 16 && nt >= 64 && nt <= kRadixMaxNt) {
+    const unsigned g = static_cast<unsigned>(m);
+    if (nt == 64) mpk::k_eu_sort_radix<T, 64, 16><<<g, 64, 0, s>>>(mags, w.pref, n, inf);
+    else if (nt == 128) mpk::k_eu_sort_radix<T, 128, 16><<<g, 128, 0, s>>>(mags, w.pref, n, inf);
+    else if (nt == 256) mpk::k_eu_sort_radix<T, 256, 16><<<g, 256, 0, s>>>(mags, w.pref, n, inf);
+    else if constexpr (sizeof(T) == 4) mpk::k_eu_sort_radix<T, 512, 16><<<g, 512, 0, s>>>(mags, w.pref, n, inf);
+    MP_CUDA_TRY(cudaGetLastError());
+  } else switch (P2 / nt) {
     case 2: MP_CUDA_TRY((launch_eu_sort<T, 2>(mags, w.pref, n, m, P2, nt, smem, inf, s))); break;
     case 4: MP_CUDA_TRY((launch_eu_sort<T, 4>(mags, w.pref, n, m, P2, nt, smem, inf, s))); break;
     case 8: MP_CUDA_TRY((launch_eu_sort<T, 8>(mags, w.pref, n, m, P2, nt, smem, inf, s))); break;
@@ -771,7 +792,10 @@ mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, doubl
   const mpk::DD* cp = w.pref;
   double* colmax = w.colmax;
   mpk::EuScratch* sc = w.sc;
-  void* args[] = {&cm, &cp, &n, &m, &eta, &colmax, &u, &inf, &sc};
+  mpk::EuLayout lay{P2, 0, 0};
+  while ((1 << lay.lge) < ek) ++lay.lge;
+  while ((1 << lay.lgnt) < nt) ++lay.lgnt;
+  void* args[] = {&cm, &cp, &n, &m, &lay, &eta, &colmax, &u, &inf, &sc};
   MP_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(mpk::k_eu_search<T>), dim3(G),
                                           dim3(mpk::kEuSearchThreads), args, 0, s));
   if (eta == 0.0) {  // the reference returns DenseTensor::zeros (+0.0 everywhere)

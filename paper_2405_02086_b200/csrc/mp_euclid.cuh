@@ -32,6 +32,8 @@
 // Sums are deterministic (fixed trees, CTA partials reduced in CTA order).
 #pragma once
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -57,10 +59,25 @@ struct EuScratch {
   long long zero[kEuMaxCtas];
 };
 
+// Sorted-column layout.  Column j occupies [j*ld, j*ld + ld), ld = P2 (the
+// sort's power of two).  Rank r (0-based, descending) of a column sorted by
+// NT threads holding E keys each (thread t: ranks t*E .. t*E+E-1) lives at
+// slot (r % E) * NT + r / E: the sort's stores -- and the unsorted loads --
+// are coalesced across a warp (rank-contiguous stores were 32 scattered
+// sectors per warp instruction).
+struct EuLayout {
+  int64_t ld;  // column stride (P2)
+  int lge;     // log2 E
+  int lgnt;    // log2 NT
+  __device__ __forceinline__ int64_t slot(int64_t r) const {
+    return ((r & ((1 << lge) - 1)) << lgnt) + (r >> lge);
+  }
+};
+
 // ------------------------------------------------------------------- EK0
 template <typename T>
 __global__ void __launch_bounds__(256) k_eu_gather(const T* __restrict__ y, int64_t n, int64_t m, T* __restrict__ mags,
-                                                   mp_info* __restrict__ info) {
+                                                   int64_t ld, mp_info* __restrict__ info) {
   __shared__ T tile[32][33];
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32, r0 = static_cast<int64_t>(blockIdx.y) * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;  // (32, 8)
@@ -79,7 +96,7 @@ __global__ void __launch_bounds__(256) k_eu_gather(const T* __restrict__ y, int6
 #pragma unroll
   for (int k = 0; k < 32; k += 8) {
     const int64_t c = c0 + ty + k, r = r0 + tx;
-    if (r < n && c < m) mags[c * n + r] = tile[tx][ty + k];
+    if (r < n && c < m) mags[c * ld + r] = tile[tx][ty + k];
   }
 }
 
@@ -108,20 +125,71 @@ __device__ __forceinline__ void bitonic_keep(T& v, T o, bool take_max) {
   v = take_max ? hi : lo;
 }
 
+// Store the sorted column and its double-double prefix sums P_k (the
+// reference's long double, euclidean.cpp:41-46): chunk totals, warp scan,
+// warp totals, block offsets, one more pass over the registers.
+template <typename T, int E>
+__device__ __forceinline__ void eu_store_prefix(const T (&v)[E], T* __restrict__ col, DD* __restrict__ pc, int64_t n,
+                                                DD* wsum) {
+  const int NT = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // rank tid*E + e -> slot e*NT + tid (EuLayout)
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = tid * E + e;
+    if (i < n) col[e * NT + tid] = v[e];
+  }
+  // prefix sums: chunk totals, warp scan, warp totals, block offsets
+  DD s{0.0, 0.0};
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if (tid * E + e < n) s = dd_add(s, static_cast<double>(v[e]));
+  DD inc = s;  // inclusive warp scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const DD w{__shfl_up_sync(0xffffffffu, inc.hi, o), __shfl_up_sync(0xffffffffu, inc.lo, o)};
+    if (lane >= o) inc = dd_add(w, inc);
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    DD t = lane < (NT >> 5) ? wsum[lane] : DD{0.0, 0.0};
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const DD w{__shfl_up_sync(0xffffffffu, t.hi, o), __shfl_up_sync(0xffffffffu, t.lo, o)};
+      if (lane >= o) t = dd_add(w, t);
+    }
+    wsum[lane] = t;  // inclusive over warps
+  }
+  __syncthreads();
+  DD run = warp > 0 ? wsum[warp - 1] : DD{0.0, 0.0};
+  const DD ex{__shfl_up_sync(0xffffffffu, inc.hi, 1), __shfl_up_sync(0xffffffffu, inc.lo, 1)};
+  if (lane > 0) run = dd_add(run, ex);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = tid * E + e;
+    if (i < n) {
+      run = dd_add(run, static_cast<double>(v[e]));
+      pc[e * NT + tid] = run;
+    }
+  }
+}
+
 template <typename T, int E>
 __global__ void __launch_bounds__(kEuSortThreads) k_eu_sort(T* __restrict__ mags, DD* __restrict__ pref, int64_t n,
                                                             int P2, const mp_info* __restrict__ info) {
+  // column stride P2 (EuLayout); the unsorted keys are read striped
+  // (coalesced): the network does not care which thread starts with which key
   if (info->status != MP_OK) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sk = reinterpret_cast<T*>(smem_raw);  // [E][NT]
   __shared__ DD wsum[32];
-  const int NT = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NT = blockDim.x, tid = threadIdx.x, lane = tid & 31;
   const int64_t j = blockIdx.x;
-  T* col = mags + j * n;
+  T* col = mags + j * P2;
   T v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const int i = tid * E + e;
+    const int i = e * NT + tid;
     v[e] = i < n ? col[i] : T(-1);  // padding sorts last
   }
   for (int k = 2; k <= P2; k <<= 1) {
@@ -163,46 +231,40 @@ __global__ void __launch_bounds__(kEuSortThreads) k_eu_sort(T* __restrict__ mags
       }
     }
   }
+  eu_store_prefix<T, E>(v, col, pref + j * P2, n, wsum);
+}
+
+// EK1 (radix): the same column sort as a CTA-wide LSD radix sort
+// (cub::BlockRadixSort over the |y| bit patterns -- non-negative floats
+// order like their bits; padding 0 sorts last among equals, so the first n
+// sorted keys are the column's), then the same prefix pass.  Blocked
+// arrangement: thread t ends with ranks t*E .. t*E+E-1, as in the bitonic
+// network; sorted values are identical, so is everything downstream.
+template <typename T, int NT, int E>
+__global__ void __launch_bounds__(NT) k_eu_sort_radix(T* __restrict__ mags, DD* __restrict__ pref, int64_t n,
+                                                      const mp_info* __restrict__ info) {
+  if (info->status != MP_OK) return;
+  using K = typename BitsT<T>::type;
+  using Sort = cub::BlockRadixSort<K, NT, E>;
+  __shared__ typename Sort::TempStorage tmp;
+  __shared__ DD wsum[32];
+  const int tid = threadIdx.x;
+  const int64_t j = blockIdx.x;
+  T* col = mags + j * (NT * E);
+  K key[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const int i = tid * E + e;
-    if (i < n) col[i] = v[e];
+    const int i = e * NT + tid;  // striped, coalesced
+    key[e] = i < n ? abs_bits(col[i]) : K(0);
   }
-  // prefix sums: chunk totals, warp scan, warp totals, block offsets
-  DD s{0.0, 0.0};
-#pragma unroll
-  for (int e = 0; e < E; ++e)
-    if (tid * E + e < n) s = dd_add(s, static_cast<double>(v[e]));
-  DD inc = s;  // inclusive warp scan
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const DD w{__shfl_up_sync(0xffffffffu, inc.hi, o), __shfl_up_sync(0xffffffffu, inc.lo, o)};
-    if (lane >= o) inc = dd_add(w, inc);
-  }
-  if (lane == 31) wsum[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    DD t = lane < (NT >> 5) ? wsum[lane] : DD{0.0, 0.0};
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const DD w{__shfl_up_sync(0xffffffffu, t.hi, o), __shfl_up_sync(0xffffffffu, t.lo, o)};
-      if (lane >= o) t = dd_add(w, t);
-    }
-    wsum[lane] = t;  // inclusive over warps
-  }
-  __syncthreads();
-  DD run = warp > 0 ? wsum[warp - 1] : DD{0.0, 0.0};
-  const DD ex{__shfl_up_sync(0xffffffffu, inc.hi, 1), __shfl_up_sync(0xffffffffu, inc.lo, 1)};
-  if (lane > 0) run = dd_add(run, ex);
-  DD* pc = pref + j * n;
+  Sort(tmp).SortDescending(key);
+  T v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const int i = tid * E + e;
-    if (i < n) {
-      run = dd_add(run, static_cast<double>(v[e]));
-      pc[i] = run;
-    }
+    if constexpr (sizeof(T) == 4) v[e] = __uint_as_float(key[e]);
+    else v[e] = __longlong_as_double(static_cast<long long>(key[e]));
   }
+  eu_store_prefix<T, E>(v, col, pref + j * (NT * E), n, wsum);
 }
 
 // ------------------------------------------------------------------- EK2
@@ -227,18 +289,21 @@ __device__ __forceinline__ double dd_div_to_double(DD a, DD b) {
 
 template <typename T>
 struct EuCol {
-  const T* a;    // sorted magnitudes, descending
-  const DD* P;   // P[k-1] = a_1 + ... + a_k
+  const T* a_;   // sorted magnitudes, descending (EuLayout slots)
+  const DD* P_;  // prefix sums P_k = a_1 + ... + a_k (EuLayout slots)
   int64_t n;
+  EuLayout L;
+  __device__ __forceinline__ T a(int64_t r) const { return a_[L.slot(r)]; }     // a_{r+1}
+  __device__ __forceinline__ DD P(int64_t r) const { return P_[L.slot(r)]; }    // P_{r+1}
   // t_k = P_k - k a_k rounded to double (euclidean.cpp:44-45), k = 1..n
   __device__ __forceinline__ double brk(int64_t k) const {
-    const DD pk = P[k - 1];
-    const double ak = static_cast<double>(a[k - 1]), kk = static_cast<double>(k);
+    const DD pk = P(k - 1);
+    const double ak = static_cast<double>(a(k - 1)), kk = static_cast<double>(k);
     const double p = kk * ak, pe = fma(kk, ak, -p);
     const DD t = dd_sub(pk, DD{p, pe});
     return t.hi + t.lo;
   }
-  __device__ __forceinline__ double total() const { const DD t = P[n - 1]; return t.hi + t.lo; }
+  __device__ __forceinline__ double total() const { const DD t = P(n - 1); return t.hi + t.lo; }
   // #{k : t_k <= theta} (the breakpoints are non-decreasing)
   __device__ __forceinline__ int64_t segment(double theta) const {
     int64_t lo = 0, hi = n;
@@ -253,7 +318,7 @@ struct EuCol {
 
 template <typename T>
 __global__ void __launch_bounds__(kEuSearchThreads)
-    k_eu_search(const T* __restrict__ mags, const DD* __restrict__ pref, int64_t n, int64_t m, double eta,
+    k_eu_search(const T* __restrict__ mags, const DD* __restrict__ pref, int64_t n, int64_t m, EuLayout lay, double eta,
                 double* __restrict__ colmax, double* __restrict__ budgets, mp_info* __restrict__ info,
                 EuScratch* __restrict__ sc) {
   namespace cg = cooperative_groups;
@@ -269,8 +334,8 @@ __global__ void __launch_bounds__(kEuSearchThreads)
   DD l1{0.0, 0.0};
   double tmax = 0.0;
   for (int64_t j = j0; j < m; j += js) {
-    const EuCol<T> c{mags + j * n, pref + j * n, n};
-    const double a1 = static_cast<double>(c.a[0]);
+    const EuCol<T> c{mags + j * lay.ld, pref + j * lay.ld, n, lay};
+    const double a1 = static_cast<double>(c.a(0));
     colmax[j] = a1;
     l1 = dd_add(l1, a1);
     tmax = fmax(tmax, c.total());
@@ -310,13 +375,13 @@ __global__ void __launch_bounds__(kEuSearchThreads)
       DD A{0.0, 0.0}, B{0.0, 0.0};
       double lo = 0.0, hi = __longlong_as_double(0x7ff0000000000000ll);
       for (int64_t j = j0; j < m; j += js) {
-        const EuCol<T> c{mags + j * n, pref + j * n, n};
+        const EuCol<T> c{mags + j * lay.ld, pref + j * lay.ld, n, lay};
         const double tot = c.total();
         if (theta >= tot) continue;  // inactive column
         int64_t k = c.segment(theta);
         if (k == 0) k = 1;
         const double kd = static_cast<double>(k);
-        A = dd_add(A, dd_div_int(c.P[k - 1], kd));
+        A = dd_add(A, dd_div_int(c.P(k - 1), kd));
         B = dd_add(B, dd_div_int(DD{1.0, 0.0}, kd));
         lo = fmax(lo, c.brk(k));
         hi = fmin(hi, k < n ? c.brk(k + 1) : tot);
@@ -360,16 +425,16 @@ __global__ void __launch_bounds__(kEuSearchThreads)
   // budgets (euclidean.cpp:143-149)
   long long zc = 0;
   for (int64_t j = j0; j < m; j += js) {
-    const EuCol<T> c{mags + j * n, pref + j * n, n};
+    const EuCol<T> c{mags + j * lay.ld, pref + j * lay.ld, n, lay};
     double u;
     if (mode == 0) {
-      u = static_cast<double>(c.a[0]);
+      u = static_cast<double>(c.a(0));
     } else if (mode == 1 || theta >= c.total()) {
       u = 0.0;
     } else {
       int64_t k = c.segment(theta);
       if (k == 0) k = 1;
-      const DD d = dd_div_int(dd_sub(c.P[k - 1], DD{theta, 0.0}), static_cast<double>(k));
+      const DD d = dd_div_int(dd_sub(c.P(k - 1), DD{theta, 0.0}), static_cast<double>(k));
       u = fmax(0.0, d.hi + d.lo);
     }
     budgets[j] = u;
