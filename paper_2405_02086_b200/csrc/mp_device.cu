@@ -741,6 +741,19 @@ cudaError_t launch_eu_sort(T* mags, mpk::DD* pref, int64_t n, int64_t m, int P2,
   return cudaGetLastError();
 }
 
+// Radix-sorted columns: CUB's temp storage is dynamic shared memory.
+template <typename T, int NT>
+cudaError_t launch_eu_radix(T* mags, mpk::DD* pref, int64_t n, int64_t m, const mp_info* inf, cudaStream_t s) {
+  using Sort = cub::BlockRadixSort<typename mpk::BitsT<T>::type, NT, 16>;
+  constexpr size_t smem = sizeof(typename Sort::TempStorage);
+  static const cudaError_t attr = cudaFuncSetAttribute(mpk::k_eu_sort_radix<T, NT, 16>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       static_cast<int>(smem));
+  if (attr != cudaSuccess) return attr;
+  mpk::k_eu_sort_radix<T, NT, 16><<<static_cast<unsigned>(m), NT, smem, s>>>(mags, pref, n, inf);
+  return cudaGetLastError();
+}
+
 template <typename T>
 mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, double eta, double* budgets,
                       mp_info* info, unsigned flags, const EuclidWs& w, cudaStream_t s) {
@@ -764,16 +777,14 @@ mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, doubl
     const char* e = std::getenv("MP_EU_SORT");
     return e && std::strcmp(e, "bitonic") == 0;
   }();
-  // (the CUB temp storage is static shared memory: <= 48 KiB -> f32 up to
-  // 512 threads, f64 up to 256)
-  constexpr int kRadixMaxNt = sizeof(T) == 4 ? 512 : 256;
-  if (!bitonic_only && ek == 16 && nt >= 64 && nt <= kRadixMaxNt) {
-    const unsigned g = static_cast<unsigned>(m);
-    if (nt == 64) mpk::k_eu_sort_radix<T, 64, 16><<<g, 64, 0, s>>>(mags, w.pref, n, inf);
-    else if (nt == 128) mpk::k_eu_sort_radix<T, 128, 16><<<g, 128, 0, s>>>(mags, w.pref, n, inf);
-    else if (nt == 256) mpk::k_eu_sort_radix<T, 256, 16><<<g, 256, 0, s>>>(mags, w.pref, n, inf);
-    else if constexpr (sizeof(T) == 4) mpk::k_eu_sort_radix<T, 512, 16><<<g, 512, 0, s>>>(mags, w.pref, n, inf);
-    MP_CUDA_TRY(cudaGetLastError());
+  if (!bitonic_only && ek == 16 && nt >= 64 && nt <= 1024) {
+    switch (nt) {
+      case 64: MP_CUDA_TRY((launch_eu_radix<T, 64>(mags, w.pref, n, m, inf, s))); break;
+      case 128: MP_CUDA_TRY((launch_eu_radix<T, 128>(mags, w.pref, n, m, inf, s))); break;
+      case 256: MP_CUDA_TRY((launch_eu_radix<T, 256>(mags, w.pref, n, m, inf, s))); break;
+      case 512: MP_CUDA_TRY((launch_eu_radix<T, 512>(mags, w.pref, n, m, inf, s))); break;
+      default: MP_CUDA_TRY((launch_eu_radix<T, 1024>(mags, w.pref, n, m, inf, s))); break;
+    }
   } else switch (P2 / nt) {
     case 2: MP_CUDA_TRY((launch_eu_sort<T, 2>(mags, w.pref, n, m, P2, nt, smem, inf, s))); break;
     case 4: MP_CUDA_TRY((launch_eu_sort<T, 4>(mags, w.pref, n, m, P2, nt, smem, inf, s))); break;

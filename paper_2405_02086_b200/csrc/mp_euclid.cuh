@@ -246,7 +246,9 @@ __global__ void __launch_bounds__(NT) k_eu_sort_radix(T* __restrict__ mags, DD* 
   if (info->status != MP_OK) return;
   using K = typename BitsT<T>::type;
   using Sort = cub::BlockRadixSort<K, NT, E>;
-  __shared__ typename Sort::TempStorage tmp;
+  // CUB's temp storage in dynamic shared memory (above 48 KiB for 1024 threads)
+  extern __shared__ __align__(16) unsigned char eu_radix_smem[];
+  typename Sort::TempStorage& tmp = *reinterpret_cast<typename Sort::TempStorage*>(eu_radix_smem);
   __shared__ DD wsum[32];
   const int tid = threadIdx.x;
   const int64_t j = blockIdx.x;
