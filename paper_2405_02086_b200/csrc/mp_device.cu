@@ -744,7 +744,7 @@ cudaError_t launch_eu_sort(T* mags, mpk::DD* pref, int64_t n, int64_t m, int P2,
 // Radix-sorted columns: CUB's temp storage is dynamic shared memory.
 template <typename T, int NT>
 cudaError_t launch_eu_radix(T* mags, mpk::DD* pref, int64_t n, int64_t m, const mp_info* inf, cudaStream_t s) {
-  using Sort = cub::BlockRadixSort<typename mpk::BitsT<T>::type, NT, 16>;
+  using Sort = cub::BlockRadixSort<typename mpk::BitsT<T>::type, NT, 16, cub::NullType, mpk::kEuRadixBits>;
   constexpr size_t smem = sizeof(typename Sort::TempStorage);
   static const cudaError_t attr = cudaFuncSetAttribute(mpk::k_eu_sort_radix<T, NT, 16>,
                                                        cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -43,6 +43,10 @@
 namespace mpk {
 
 constexpr int kEuSortThreads = 1024;
+#ifndef MP_EU_RADIX_BITS
+#define MP_EU_RADIX_BITS 4
+#endif
+constexpr int kEuRadixBits = MP_EU_RADIX_BITS;  // digit width of the column radix sort
 constexpr int kEuSearchThreads = 256;
 constexpr int kEuMaxCtas = 1024;
 constexpr size_t kEuSortSmemMax = 200 * 1024;
@@ -245,7 +249,7 @@ __global__ void __launch_bounds__(NT) k_eu_sort_radix(T* __restrict__ mags, DD* 
                                                       const mp_info* __restrict__ info) {
   if (info->status != MP_OK) return;
   using K = typename BitsT<T>::type;
-  using Sort = cub::BlockRadixSort<K, NT, E>;
+  using Sort = cub::BlockRadixSort<K, NT, E, cub::NullType, kEuRadixBits>;
   // CUB's temp storage in dynamic shared memory (above 48 KiB for 1024 threads)
   extern __shared__ __align__(16) unsigned char eu_radix_smem[];
   typename Sort::TempStorage& tmp = *reinterpret_cast<typename Sort::TempStorage*>(eu_radix_smem);
@@ -259,7 +263,8 @@ __global__ void __launch_bounds__(NT) k_eu_sort_radix(T* __restrict__ mags, DD* 
     const int i = e * NT + tid;  // striped, coalesced
     key[e] = i < n ? abs_bits(col[i]) : K(0);
   }
-  Sort(tmp).SortDescending(key);
+  // magnitudes: the sign bit is always clear, sort the low 31 / 63 bits
+  Sort(tmp).SortDescending(key, 0, static_cast<int>(sizeof(K) * 8 - 1));
   T v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
