@@ -174,7 +174,7 @@ int64_t max_nrb(mp_dtype dt, int64_t n, int64_t m) {
 inline int k1_row_groups(int tx) { return tx >= 128 ? 1 : std::min(16, 1024 / tx); }
 
 template <typename T, int VEC, int Q, bool RG>
-cudaError_t launch_colnorm_rg(int64_t n, int64_t m, const T* y, void* out, Grid& g, cudaStream_t s) {
+cudaError_t launch_colnorm_rg(int64_t n, int64_t m, const T* y, void* out, Grid& g, cudaStream_t s, int ncopy) {
   constexpr int U = (sizeof(T) * VEC == 32) ? 4 : 8;  // 128 bytes of loads in flight per thread
   auto fn = mpk::k_colnorm<T, VEC, Q, U, RG>;
   const int tx = threads_for(VEC, m);
@@ -187,32 +187,34 @@ cudaError_t launch_colnorm_rg(int64_t n, int64_t m, const T* y, void* out, Grid&
   const int64_t slots = g.nrb * ty;
   const int64_t rpb = kRowInterleave ? n / slots : (n + slots - 1) / slots;
   dim3 grid(static_cast<unsigned>(g.ntiles), static_cast<unsigned>(g.nrb));
-  fn<<<grid, dim3(tx, ty), smem, s>>>(y, n, m, rpb, kRowInterleave, out);
+  fn<<<grid, dim3(tx, ty), smem, s>>>(y, n, m, rpb, kRowInterleave, out, ncopy);
   return cudaGetLastError();
 }
 
 template <typename T, int VEC, int Q>
-cudaError_t launch_colnorm_q(int64_t n, int64_t m, const T* y, void* out, Grid& g, cudaStream_t s) {
-  if (k1_row_groups(threads_for(VEC, m)) > 1) return launch_colnorm_rg<T, VEC, Q, true>(n, m, y, out, g, s);
-  return launch_colnorm_rg<T, VEC, Q, false>(n, m, y, out, g, s);
+cudaError_t launch_colnorm_q(int64_t n, int64_t m, const T* y, void* out, Grid& g, cudaStream_t s, int ncopy) {
+  if (k1_row_groups(threads_for(VEC, m)) > 1) return launch_colnorm_rg<T, VEC, Q, true>(n, m, y, out, g, s, ncopy);
+  return launch_colnorm_rg<T, VEC, Q, false>(n, m, y, out, g, s, ncopy);
 }
 
 template <typename T, int VEC>
-cudaError_t launch_colnorm_v(int q, const T* y, int64_t n, int64_t m, void* out, Grid& g, cudaStream_t s) {
-  if (q == mpk::kInf) return launch_colnorm_q<T, VEC, mpk::kInf>(n, m, y, out, g, s);
-  if (q == mpk::kL1) return launch_colnorm_q<T, VEC, mpk::kL1>(n, m, y, out, g, s);
-  return launch_colnorm_q<T, VEC, mpk::kL2>(n, m, y, out, g, s);
+cudaError_t launch_colnorm_v(int q, const T* y, int64_t n, int64_t m, void* out, Grid& g, cudaStream_t s,
+                             int ncopy) {
+  if (q == mpk::kInf) return launch_colnorm_q<T, VEC, mpk::kInf>(n, m, y, out, g, s, ncopy);
+  if (q == mpk::kL1) return launch_colnorm_q<T, VEC, mpk::kL1>(n, m, y, out, g, s, 1);
+  return launch_colnorm_q<T, VEC, mpk::kL2>(n, m, y, out, g, s, 1);
 }
 
 // K1; `g` returns the grid used (g.nrb = number of l1/l2 partial rows).
 template <typename T>
-cudaError_t launch_colnorm(int q, int vec, const T* y, int64_t n, int64_t m, void* out, Grid& g, cudaStream_t s) {
+cudaError_t launch_colnorm(int q, int vec, const T* y, int64_t n, int64_t m, void* out, Grid& g, cudaStream_t s,
+                           int ncopy = 1) {
   if (vec == 8) {
-    if constexpr (sizeof(T) == 4) return launch_colnorm_v<T, 8>(q, y, n, m, out, g, s);
+    if constexpr (sizeof(T) == 4) return launch_colnorm_v<T, 8>(q, y, n, m, out, g, s, ncopy);
   }
-  if (vec == 4) return launch_colnorm_v<T, 4>(q, y, n, m, out, g, s);
-  if (vec == 2) return launch_colnorm_v<T, 2>(q, y, n, m, out, g, s);
-  return launch_colnorm_v<T, 1>(q, y, n, m, out, g, s);
+  if (vec == 4) return launch_colnorm_v<T, 4>(q, y, n, m, out, g, s, ncopy);
+  if (vec == 2) return launch_colnorm_v<T, 2>(q, y, n, m, out, g, s, ncopy);
+  return launch_colnorm_v<T, 1>(q, y, n, m, out, g, s, ncopy);
 }
 
 template <typename T, int VEC, int Q>
@@ -290,14 +292,18 @@ cudaError_t launch_outer_p(const mpk::OuterArgs& a, int C, int chunk, cudaStream
   return cudaLaunchKernelEx(&cfg, mpk::k_outer<P>, a);
 }
 
-template <int P, int NT = mpk::kOuterRegThreads>
+template <int P, int NT = mpk::kOuterRegThreads, bool FOLD = false>
 cudaError_t launch_outer_reg(const mpk::OuterArgs& a, cudaStream_t s) {
-  return launch_pdl(mpk::k_outer_reg<P, NT>, dim3(1), dim3(NT), 0, s, a);
+  return launch_pdl(mpk::k_outer_reg<P, NT, FOLD>, dim3(1), dim3(NT), 0, s, a);
 }
 
 cudaError_t launch_outer(const mpk::OuterArgs& a, cudaStream_t s) {
   cudaError_t e = outer_setup();
   if (e != cudaSuccess) return e;
+  if (a.ncopy > 1) {  // narrow l_inf: fold K1's copies of the maxima (m <= 512)
+    if (a.m <= 256) return launch_outer_reg<1, 256, true>(a, s);
+    return launch_outer_reg<2, 256, true>(a, s);
+  }
   if (a.m <= 2048) {  // small vectors: a 256-thread CTA, cheaper barriers
     const int64_t per = (std::max<int64_t>(a.m, 1) + 255) / 256;
     if (per <= 1) return launch_outer_reg<1, 256>(a, s);
@@ -345,6 +351,11 @@ __global__ void k_colparams(const double* __restrict__ v, const double* __restri
   }
 }
 
+// Narrow l_inf matrices (m <= 512, K2 = k_outer_reg<P, 256, true>, which
+// folds the copies): K1's atomics spread over 8 copies of the maxima
+// (256^3 tri-level: 148 same-address atomics per column -> 19).
+inline int inf_copies(int64_t m) { return m <= 512 ? mpk::kInfCopies : 1; }
+
 // ------------------------------------------------------ workspace layouts
 struct BilevelWs {
   mp_info* info;
@@ -360,7 +371,8 @@ struct BilevelWs {
 BilevelWs carve_bilevel(Carve& c, mp_dtype dt, int64_t n, int64_t m, mp_norm q) {
   BilevelWs w{};
   w.info = c.take<mp_info>(1);
-  if (q == MP_NORM_INF) w.k1out = c.take<unsigned long long>(m);
+  // l_inf: bit-pattern maxima, kInfCopies copies for narrow matrices
+  if (q == MP_NORM_INF) w.k1out = c.take<unsigned long long>(static_cast<size_t>(inf_copies(m)) * m);
   else w.k1out = c.take<double>(static_cast<size_t>(max_nrb(dt, n, m)) * m);
   w.v = c.take<double>(m);
   w.budgets = c.take<double>(m);
@@ -430,8 +442,10 @@ mp_status bilevel_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, mp_n
   A.u_out = u;
   A.info_w = inf;
   if (q == MP_NORM_INF) {
-    MP_CUDA_TRY(cudaMemsetAsync(w.k1out, 0, static_cast<size_t>(m) * sizeof(unsigned long long), s));
-    MP_CUDA_TRY(launch_colnorm<T>(q, vec, y, n, m, w.k1out, g, s));
+    const int ncopy = inf_copies(m);
+    MP_CUDA_TRY(cudaMemsetAsync(w.k1out, 0, static_cast<size_t>(ncopy) * m * sizeof(T), s));
+    MP_CUDA_TRY(launch_colnorm<T>(q, vec, y, n, m, w.k1out, g, s, ncopy));
+    oa.ncopy = ncopy;
     oa.vin = w.k1out;
     oa.vkind = sizeof(T) == 4 ? 0 : 1;  // f64 |y| bits are the f64 values
     A.v = w.k1out;

@@ -174,9 +174,13 @@ __device__ __forceinline__ RowWalk row_walk(int64_t n, int64_t rpb, int interlea
 // threads) stack up to 16 row groups in one CTA and fold them in shared
 // memory first, so each column sees one atomic / partial per CTA instead of
 // one per row group (atomics on few addresses serialise in L2).
+// l_inf: CTA row block r folds into copy r % ncopy of the maxima (narrow
+// matrices: fewer same-address atomics serialised in one L2 slice; K2 folds
+// the copies).
 template <typename T, int VEC, int Q, int U, bool RG>
 __global__ void __launch_bounds__(RG ? 1024 : kThreads, RG ? 1 : 8)
-    k_colnorm(const T* __restrict__ y, int64_t n, int64_t m, int64_t rpb, int interleave, void* __restrict__ out) {
+    k_colnorm(const T* __restrict__ y, int64_t n, int64_t m, int64_t rpb, int interleave, void* __restrict__ out,
+              int ncopy) {
   pdl_trigger();  // let the (single-CTA) outer kernel be scheduled as SMs free up
   tl_begin(0);
   const int64_t c0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * VEC;
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(RG ? 1024 : kThreads, RG ? 1 : 8)
         for (int j = 0; j < VEC; ++j) acc[j] = max(acc[j], red[(r * blockDim.x + threadIdx.x) * VEC + j]);
     }
     if (RG && !active) return;
-    B* vb = static_cast<B*>(out) + c0;
+    B* vb = static_cast<B*>(out) + static_cast<int64_t>(blockIdx.y % ncopy) * m + c0;
 #pragma unroll
     for (int j = 0; j < VEC; ++j) atomicMax(vb + j, acc[j]);
     tl_end(0);
@@ -456,7 +460,35 @@ struct OuterArgs {
   void* scratch;     // k_outer_large only: LargeScratch in the workspace
   OuterParams* params;  // nullable: mode / tau / scale for derive_u
   int emit;          // 1: write the per-element outputs above; 0: params + info only
+  int ncopy;         // kInfCopies: fold K1's copies of the maxima (k_outer_reg<P, 256, true>); else one
 };
+
+// Fold the kInfCopies copies of K1's bit-pattern maxima for element i (max
+// is order-free; all loads in flight) and leave the result in copy 0 for the
+// apply pass.
+constexpr int kInfCopies = 8;
+__device__ __forceinline__ double outer_load_fold(const OuterArgs& a, int64_t i) {
+  if (a.vkind == 0) {
+    unsigned* b = static_cast<unsigned*>(const_cast<void*>(a.vin));
+    unsigned c8[kInfCopies];
+#pragma unroll
+    for (int c = 0; c < kInfCopies; ++c) c8[c] = b[c * a.m + i];
+    unsigned mx = c8[0];
+#pragma unroll
+    for (int c = 1; c < kInfCopies; ++c) mx = max(mx, c8[c]);
+    b[i] = mx;
+    return static_cast<double>(__uint_as_float(mx));
+  }
+  unsigned long long* b = static_cast<unsigned long long*>(const_cast<void*>(a.vin));
+  unsigned long long c8[kInfCopies];
+#pragma unroll
+  for (int c = 0; c < kInfCopies; ++c) c8[c] = b[c * a.m + i];
+  unsigned long long mx = c8[0];
+#pragma unroll
+  for (int c = 1; c < kInfCopies; ++c) mx = max(mx, c8[c]);
+  b[i] = mx;
+  return __longlong_as_double(static_cast<long long>(mx));
+}
 
 __device__ __forceinline__ void outer_publish(const OuterArgs& a, int mode, double tau, double scale) {
   if (a.params) {
@@ -726,7 +758,7 @@ constexpr int64_t kOuterRegMaxM = static_cast<int64_t>(kOuterRegThreads) * kOute
 // registers (P per thread, compile time), every reduction a single-barrier
 // all-reduce.  The kernel's time is its dependency chain on one SM: a load
 // wave, 1 + passes + 1 block reductions, one double division per pass.
-template <int P, int NT = kOuterRegThreads>
+template <int P, int NT = kOuterRegThreads, bool FOLD = false>
 __global__ void __launch_bounds__(NT, 1) k_outer_reg(OuterArgs a) {
   pdl_wait();
   pdl_trigger();
@@ -744,7 +776,7 @@ __global__ void __launch_bounds__(NT, 1) k_outer_reg(OuterArgs a) {
 #pragma unroll
   for (int j = 0; j < P; ++j) {
     const int i = tid + j * NT;
-    v[j] = (i < m) ? outer_load(a, i) : 0.0;
+    v[j] = (i < m) ? (FOLD ? outer_load_fold(a, i) : outer_load(a, i)) : 0.0;
   }
   int nzero = 0;
 #pragma unroll
