@@ -217,10 +217,9 @@ cudaError_t launch_colnorm(int q, int vec, const T* y, int64_t n, int64_t m, voi
   return launch_colnorm_v<T, 1>(q, y, n, m, out, g, s, ncopy);
 }
 
-template <typename T, int VEC, int Q>
-cudaError_t launch_apply_q(const T* y, T* x, int64_t n, int64_t m, const mpk::ApplyCols& A, bool derive,
-                           const mp_info* info, unsigned flags, cudaStream_t s) {
-  constexpr int U = Q == mpk::kInf ? 8 : 4;  // l_inf: 8 packs in flight per thread (c2 K3 ~130 -> 127 us)
+template <typename T, int VEC, int Q, int U>
+cudaError_t launch_apply_qu(const T* y, T* x, int64_t n, int64_t m, const mpk::ApplyCols& A, bool derive,
+                            const mp_info* info, unsigned flags, cudaStream_t s) {
   const int t = threads_for(VEC, m);
   const void* fn = derive ? reinterpret_cast<const void*>(mpk::k_apply<T, VEC, Q, U, true>)
                           : reinterpret_cast<const void*>(mpk::k_apply<T, VEC, Q, U, false>);
@@ -233,6 +232,20 @@ cudaError_t launch_apply_q(const T* y, T* x, int64_t n, int64_t m, const mpk::Ap
   return launch_pdl(mpk::k_apply<T, VEC, Q, U, false>, grid, dim3(g.threads), 0, s, y, x, n, m,
                       kRowInterleave ? n / g.nrb : g.rpb, kRowInterleave, A, info,
                     flags);
+}
+
+// l_inf: 8 packs in flight per thread (config 2 K3 ~130 -> 127 us) when the
+// row slots are deep enough to fill batches of 8 (short matrices keep 4: one
+// HBM round trip for their few rows, config 1 K3 3.8 -> 2.8 us).
+template <typename T, int VEC, int Q>
+cudaError_t launch_apply_q(const T* y, T* x, int64_t n, int64_t m, const mpk::ApplyCols& A, bool derive,
+                           const mp_info* info, unsigned flags, cudaStream_t s) {
+  if constexpr (Q == mpk::kInf) {
+    const int t = threads_for(VEC, m);
+    const Grid g8 = plan_grid(VEC, n, m, occupancy(reinterpret_cast<const void*>(mpk::k_apply<T, VEC, Q, 8, true>), t));
+    if (n / g8.nrb >= 16) return launch_apply_qu<T, VEC, Q, 8>(y, x, n, m, A, derive, info, flags, s);
+  }
+  return launch_apply_qu<T, VEC, Q, 4>(y, x, n, m, A, derive, info, flags, s);
 }
 
 template <typename T, int VEC>
