@@ -49,10 +49,15 @@ for rel in [float(r) for r in os.environ.get("RELS", "0.001,0.5").split(",")]:
         t0 = t[0]
         rel_t = [(t[i] - t0) / 1e3 if t[i] not in (0, 2**63 - 1) else float("nan") for i in range(8)]
         res.append(rel_t + [e0.elapsed_time(e1) * 1e3])
-        extra = t[8:15]
+        extra = t[8:16]
     if extra[2] > 0:
         print(f"  l1: mean passes {extra[0] / extra[2]:.2f} per strip ({extra[3] / extra[2]:.2f} exact) over"
-              f" {extra[2]:.0f} strips; max per CTA {extra[1]:.0f}; aux slots {extra[4]:.0f} {extra[5]:.0f} {extra[6]:.0f}")
+              f" {extra[2]:.0f} strips; max per CTA {extra[1]:.0f}")
+        tot = extra[4] + extra[5] + extra[6]
+        if tot > 0:
+            print(f"  l1 CTA cycles: wait-for-strip {extra[4] / tot:.1%}  passes {extra[5] / tot:.1%}  "
+                  f"apply {extra[6] / tot:.1%}  (per strip: {extra[4] / extra[2]:.0f} / {extra[5] / extra[2]:.0f} / "
+                  f"{extra[6] / extra[2]:.0f} cycles)")
     inf_ = p.info()
     print(f"  info: iterations={inf_.iterations} survivors={inf_.survivors} zero_columns={inf_.zero_columns}")
     r = np.median(np.array(res), axis=0)
