@@ -38,6 +38,7 @@
 // would see its count repeat.  Otherwise the exact step continues from t_ex.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <type_traits>
@@ -160,16 +161,58 @@ __device__ __forceinline__ uint4 reg_pack(const T (&e)[16 / sizeof(T)]) {
   }
 }
 
-template <typename T, int P, bool DERIVE, bool PERSIST, int NT = kRegThreads, int RS = 0>
+// TMA (cp.async.bulk.tensor) helpers for the shared-memory half of a hybrid
+// strip: 2-D boxes of 8 columns x 256 rows move between global memory and
+// the [rows][8] shared-memory layout, which for P = 2, NT = 256 is exactly
+// the thread-private slot layout sq[i * NT + tid] (thread t holds row
+// t / 2, 16-byte half t % 2).  The copies bypass the LSU: a 32-byte-wide
+// strip row costs one L1 transaction per row piece on the LSU path.
+struct TmaMaps {
+  CUtensorMap y, x;
+};
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, int c0, int c1, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];"
+               ::"l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+
+template <typename T, int P, bool DERIVE, bool PERSIST, int NT = kRegThreads, int RS = 0, bool TMA = false>
 __global__ void __launch_bounds__(NT, kRegThreads / NT)
     k_l1reg(const T* __restrict__ y, T* __restrict__ x, int n, int64_t m, const double* __restrict__ v,
             const double* __restrict__ u, double* __restrict__ tau_out, const mp_info* __restrict__ info,
-            const OuterParams* __restrict__ params, double* __restrict__ u_out, int64_t nstrips) {
+            const OuterParams* __restrict__ params, double* __restrict__ u_out, int64_t nstrips,
+            const __grid_constant__ TmaMaps tm) {
   constexpr int C4 = 16 / sizeof(T);
   constexpr int W = C4 * P;  // strip columns
   constexpr int NW = NT / 32;
   constexpr int SL = NT / P;  // row slots
-  constexpr int RPT = kRegRPT;
+  // TMA strips keep 32 - RS pieces per thread in registers (the rest in
+  // shared memory, moved by TMA); the others kRegRPT
+  constexpr int RPT = TMA ? 32 - RS : kRegRPT;
   constexpr bool kF32 = sizeof(T) == 4;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int64_t strip = blockIdx.x;
@@ -180,10 +223,29 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
   // RS > 0: the strip's last RS pieces per thread live in shared memory
   // ([RS][NT] uint4, each thread lands and reads back only its own), the
   // first RPT in registers -- half the registers per strip, two CTAs per SM.
-  extern __shared__ __align__(16) uint4 sq[];
+  extern __shared__ __align__(128) uint4 sq[];
   constexpr int NPC = RPT + RS;  // pieces per thread
+  static_assert(!TMA || (RS > 0 && P == 2 && NT == 256 && sizeof(T) == 4), "TMA strips: f32, P = 2, 256 threads");
+  constexpr int kBoxRows = 256, kBoxes = RS * SL / kBoxRows;
+  __shared__ unsigned long long mbar;
+  unsigned mph = 0;  // mbarrier phase of the next landing
+  if constexpr (TMA) {
+    if (tid == 0) {
+      mbar_init(&mbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   auto land_smem = [&](int64_t s_strip) {
-    if constexpr (RS > 0) {
+    if constexpr (TMA) {
+      if (tid == 0) {
+        mbar_expect(&mbar, static_cast<unsigned>(RS * NT * 16));
+#pragma unroll
+        for (int b = 0; b < kBoxes; ++b)
+          tma_load_2d(reinterpret_cast<char*>(sq) + b * kBoxRows * W * sizeof(T), &tm.y,
+                      static_cast<int>(s_strip * W), SL * RPT + b * kBoxRows, &mbar);
+      }
+    } else if constexpr (RS > 0) {
       const T* yp = y + static_cast<int64_t>(rb + SL * RPT) * m + s_strip * W + pc;
 #pragma unroll
       for (int i = 0; i < RS; ++i, yp += step) {
@@ -246,7 +308,12 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
       if (DERIVE && u_out && warp == 0) u_out[strip * W + lane] = ul;
     }
     const bool any_proj = __any_sync(0xffffffffu, pj);
-    if constexpr (RS > 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if constexpr (TMA) {
+      mbar_wait(&mbar, mph);
+      mph ^= 1u;
+    } else if constexpr (RS > 0) {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
 
     if (any_proj) {
       bool xp = false;  // exact pass (CTA-uniform)
@@ -411,14 +478,31 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
                                   static_cast<UT>(__double_as_longlong(e[c])) & keep[c]));
           }
         }
-        __stcs(reinterpret_cast<uint4*>(xq), reg_pack<T>(e));
+        if (TMA && i >= RPT) sq[(i >= RPT ? i - RPT : 0) * NT + tid] = reg_pack<T>(e);  // TMA stores it
+        else __stcs(reinterpret_cast<uint4*>(xq), reg_pack<T>(e));
       }
       if (more) {
         if (i < RPT) q[i < RPT ? i : 0] = __ldg(reinterpret_cast<const uint4*>(yn));
-        else if constexpr (RS > 0) cp_async_16(&sq[(i - RPT) * NT + tid], yn);
+        else if constexpr (RS > 0 && !TMA) cp_async_16(&sq[(i - RPT) * NT + tid], yn);
       }
     }
-    if constexpr (RS > 0) {
+    if constexpr (TMA) {
+      // the shared-memory half goes out by TMA; once the engine has read it,
+      // the next strip's half lands in the same buffer
+      if (need_store) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        if (need_store) {
+#pragma unroll
+          for (int b = 0; b < kBoxes; ++b)
+            tma_store_2d(&tm.x, static_cast<int>(strip * W), SL * RPT + b * kBoxRows,
+                         reinterpret_cast<const char*>(sq) + b * kBoxRows * W * sizeof(T));
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        if (more) land_smem(next);
+      }
+    } else if constexpr (RS > 0) {
       if (more) {
         // rows past n of the next strip: zero pieces (none when n fills the slots)
 #pragma unroll
@@ -436,6 +520,9 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
     atomicMax(g_mp_timeline + 9, static_cast<unsigned long long>(npass));
     atomicAdd(g_mp_timeline + 10, static_cast<unsigned long long>(nst));
   }
+  if constexpr (TMA) {
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
+  }
   tl_end(3);
 }
 
@@ -450,6 +537,7 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
 // 1000x16384 74 -> 56; 2000x32768 240 -> 211; 4096x16384 255 -> 206 (hybrid,
 // 2 CTAs per SM); 6000x8192 201 us.  P = 0 when the path does not apply.
 constexpr int kRegHybridRS = 16;
+constexpr int kRegTmaRS = 24;  // TMA strips: 24 of 32 pieces in shared memory (96 KiB per CTA)
 struct RegGeom {
   int P = 0, NT = 0, RS = 0;
 };

@@ -218,21 +218,57 @@ inline int l1reg_prefer_p() {
   return p;
 }
 
+// TMA maps for the hybrid strips' shared-memory half (f32, 8-column x
+// 256-row boxes over the (n, m) row-major matrix).  The encoder comes from
+// the driver through the runtime (no libcuda link).  MP_L1_TMA=0 keeps the
+// cp.async / LSU path (A/B aid).
+inline bool l1_tma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MP_L1_TMA");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+inline bool encode_strip_map(CUtensorMap* tm, const void* base, int64_t n, int64_t m) {
+  typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                          const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Enc enc = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<Enc>(fn);
+  }();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(n)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(m) * 4};
+  const cuuint32_t box[2] = {8, 256};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Grid-stride CTAs, as many as are co-resident (kRegThreads / NT per SM).
-template <typename T, int P, int NT, int RS = 0>
+template <typename T, int P, int NT, int RS = 0, bool TMA = false>
 cudaError_t launch_reg(const T* y, T* x, int64_t n, int64_t m, const double* v, const double* u,
-                       const L1StripWs& ws, const mp_info* info, const L1Derive& dv, cudaStream_t s) {
+                       const L1StripWs& ws, const mp_info* info, const L1Derive& dv, cudaStream_t s,
+                       const TmaMaps* maps = nullptr) {
   constexpr int W = 16 / sizeof(T) * P;
   const int64_t nstrips = m / W;
   const size_t smem = static_cast<size_t>(NT) * RS * 16;
   if constexpr (RS > 0) {
-    static const cudaError_t a1 = cudaFuncSetAttribute(k_l1reg<T, P, true, true, NT, RS>,
+    static const cudaError_t a1 = cudaFuncSetAttribute(k_l1reg<T, P, true, true, NT, RS, TMA>,
                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    static const cudaError_t a2 = cudaFuncSetAttribute(k_l1reg<T, P, false, true, NT, RS>,
+    static const cudaError_t a2 = cudaFuncSetAttribute(k_l1reg<T, P, false, true, NT, RS, TMA>,
                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (a1 != cudaSuccess) return a1;
     if (a2 != cudaSuccess) return a2;
   }
+  TmaMaps tm{};
+  if (maps) tm = *maps;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(NT);
   cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(nstrips, static_cast<int64_t>(mpi::sm_count()) *
@@ -245,10 +281,10 @@ cudaError_t launch_reg(const T* y, T* x, int64_t n, int64_t m, const double* v, 
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (dv.params)
-    return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, true, true, NT, RS>, y, x, static_cast<int>(n), m, v, u, ws.tau,
-                              info, dv.params, dv.u_out, nstrips);
-  return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, false, true, NT, RS>, y, x, static_cast<int>(n), m, v, u, ws.tau,
-                            info, dv.params, dv.u_out, nstrips);
+    return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, true, true, NT, RS, TMA>, y, x, static_cast<int>(n), m, v, u,
+                              ws.tau, info, dv.params, dv.u_out, nstrips, tm);
+  return cudaLaunchKernelEx(&cfg, k_l1reg<T, P, false, true, NT, RS, TMA>, y, x, static_cast<int>(n), m, v, u,
+                            ws.tau, info, dv.params, dv.u_out, nstrips, tm);
 }
 
 template <typename T, int P>
@@ -257,7 +293,17 @@ cudaError_t launch_reg_nt(const RegGeom& g, const T* y, T* x, int64_t n, int64_t
   if constexpr (P == 2) {
     if (g.RS > 0) {
       if (g.NT == 128) return launch_reg<T, 2, 128, kRegHybridRS>(y, x, n, m, v, u, ws, info, dv, s);
-      if (g.NT == 256) return launch_reg<T, 2, 256, kRegHybridRS>(y, x, n, m, v, u, ws, info, dv, s);
+      if (g.NT == 256) {
+        if constexpr (sizeof(T) == 4) {
+          // TMA for the shared-memory half (16-byte-aligned rows, n <= 4096)
+          TmaMaps maps{};
+          if (l1_tma_enabled() && reinterpret_cast<uintptr_t>(y) % 16 == 0 &&
+              reinterpret_cast<uintptr_t>(x) % 16 == 0 && encode_strip_map(&maps.y, y, n, m) &&
+              encode_strip_map(&maps.x, x, n, m))
+            return launch_reg<T, 2, 256, kRegTmaRS, true>(y, x, n, m, v, u, ws, info, dv, s, &maps);
+        }
+        return launch_reg<T, 2, 256, kRegHybridRS>(y, x, n, m, v, u, ws, info, dv, s);
+      }
       return launch_reg<T, 2, kRegThreads, kRegHybridRS>(y, x, n, m, v, u, ws, info, dv, s);
     }
   }
