@@ -229,6 +229,7 @@ inline bool l1_tma_enabled() {
   }();
   return on;
 }
+template <typename T>
 inline bool encode_strip_map(CUtensorMap* tm, const void* base, int64_t n, int64_t m) {
   typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                           const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -243,10 +244,11 @@ inline bool encode_strip_map(CUtensorMap* tm, const void* base, int64_t n, int64
   }();
   if (!enc) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(n)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(m) * 4};
-  const cuuint32_t box[2] = {8, 256};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(m) * sizeof(T)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(32 / sizeof(T)), 256};  // 32-byte strip rows
   const cuuint32_t es[2] = {1, 1};
-  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+  return enc(tm, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+             const_cast<void*>(base), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -294,12 +296,12 @@ cudaError_t launch_reg_nt(const RegGeom& g, const T* y, T* x, int64_t n, int64_t
     if (g.RS > 0) {
       if (g.NT == 128) return launch_reg<T, 2, 128, kRegHybridRS>(y, x, n, m, v, u, ws, info, dv, s);
       if (g.NT == 256) {
-        if constexpr (sizeof(T) == 4) {
-          // TMA for the shared-memory half (16-byte-aligned rows, n <= 4096)
+        {
+          // TMA for the shared-memory pieces (16-byte-aligned rows, n <= 4096)
           TmaMaps maps{};
           if (l1_tma_enabled() && reinterpret_cast<uintptr_t>(y) % 16 == 0 &&
-              reinterpret_cast<uintptr_t>(x) % 16 == 0 && encode_strip_map(&maps.y, y, n, m) &&
-              encode_strip_map(&maps.x, x, n, m))
+              reinterpret_cast<uintptr_t>(x) % 16 == 0 && encode_strip_map<T>(&maps.y, y, n, m) &&
+              encode_strip_map<T>(&maps.x, x, n, m))
             return launch_reg<T, 2, 256, kRegTmaRS, true>(y, x, n, m, v, u, ws, info, dv, s, &maps);
         }
         return launch_reg<T, 2, 256, kRegHybridRS>(y, x, n, m, v, u, ws, info, dv, s);
