@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
   // first RPT in registers -- half the registers per strip, two CTAs per SM.
   extern __shared__ __align__(128) uint4 sq[];
   constexpr int NPC = RPT + RS;  // pieces per thread
-  static_assert(!TMA || (RS > 0 && P == 2 && NT == 256), "TMA strips: P = 2 (32-byte rows), 256 threads");
+  static_assert(!TMA || (RS > 0 && P == 2 && (NT == 128 || NT == 256)), "TMA strips: P = 2 (32-byte rows), 128/256 threads");
   constexpr int kBoxRows = 256, kBoxes = RS * SL / kBoxRows;
   __shared__ unsigned long long mbar;
   unsigned mph = 0;  // mbarrier phase of the next landing
@@ -495,8 +495,7 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
         // four store groups: each quarter's boxes reload as soon as the
         // engine has read them, while the later quarters are still being
         // read (one group: 179 us on config 3, two or four: 173 us)
-        constexpr int kQ = kBoxes / 4;
-        static_assert(kBoxes % 4 == 0, "four store groups");
+        constexpr int kQ = kBoxes / 4;  // groups [0,kQ) [kQ,2kQ) [2kQ,3kQ) [3kQ,kBoxes)
         auto store = [&](int b0, int b1) {
           for (int b = b0; b < b1; ++b)
             tma_store_2d(&tm.x, static_cast<int>(strip * W), SL * RPT + b * kBoxRows,
