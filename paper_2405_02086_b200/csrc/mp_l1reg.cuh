@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
   // first RPT in registers -- half the registers per strip, two CTAs per SM.
   extern __shared__ __align__(128) uint4 sq[];
   constexpr int NPC = RPT + RS;  // pieces per thread
-  static_assert(!TMA || (RS > 0 && P == 2 && (NT == 128 || NT == 256)), "TMA strips: P = 2 (32-byte rows), 128/256 threads");
+  static_assert(!TMA || (RS > 0 && P == 2), "TMA strips: P = 2 (32-byte rows)");
   constexpr int kBoxRows = 256, kBoxes = RS * SL / kBoxRows;
   __shared__ unsigned long long mbar;
   unsigned mph = 0;  // mbarrier phase of the next landing

@@ -306,6 +306,13 @@ cudaError_t launch_reg_nt(const RegGeom& g, const T* y, T* x, int64_t n, int64_t
         }
         return launch_reg<T, 2, 256, kRegHybridRS>(y, x, n, m, v, u, ws, info, dv, s);
       }
+      if constexpr (sizeof(T) == 8) {  // f64, 4097..8192 rows: 512-thread TMA strips
+        TmaMaps maps{};
+        if (l1_tma_enabled() && reinterpret_cast<uintptr_t>(y) % 16 == 0 &&
+            reinterpret_cast<uintptr_t>(x) % 16 == 0 && encode_strip_map<T>(&maps.y, y, n, m) &&
+            encode_strip_map<T>(&maps.x, x, n, m))
+          return launch_reg<T, 2, kRegThreads, kRegTmaRS, true>(y, x, n, m, v, u, ws, info, dv, s, &maps);
+      }
       return launch_reg<T, 2, kRegThreads, kRegHybridRS>(y, x, n, m, v, u, ws, info, dv, s);
     }
   }
