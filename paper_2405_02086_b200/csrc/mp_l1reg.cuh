@@ -226,6 +226,7 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
   extern __shared__ __align__(128) uint4 sq[];
   constexpr int NPC = RPT + RS;  // pieces per thread
   static_assert(!TMA || (RS > 0 && P == 2), "TMA strips: P = 2 (32-byte rows)");
+  static_assert(!TMA || (RS * (NT / P)) % 256 == 0, "TMA strips: whole 256-row boxes");
   constexpr int kBoxRows = 256, kBoxes = RS * SL / kBoxRows;
   __shared__ unsigned long long mbar;
   unsigned mph = 0;  // mbarrier phase of the next landing
@@ -558,7 +559,10 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
 // 1000x16384 74 -> 56; 2000x32768 240 -> 211; 4096x16384 255 -> 206 (hybrid,
 // 2 CTAs per SM); 6000x8192 201 us.  P = 0 when the path does not apply.
 constexpr int kRegHybridRS = 16;
-constexpr int kRegTmaRS = 24;  // TMA strips: 24 of 32 pieces in shared memory (96 KiB per CTA)
+// TMA strips: shared-memory pieces per thread (of 32).  RS * (NT / 2) rows
+// must be whole 256-row boxes -- the mbarrier expects RS * NT * 16 bytes.
+// 256 / 512 threads: 26 (config 3 K3b 172.8 -> 169.5 us vs 24); 128: 24.
+constexpr int tma_rs(int nt) { return nt == 128 ? 24 : 26; }
 struct RegGeom {
   int P = 0, NT = 0, RS = 0;
 };

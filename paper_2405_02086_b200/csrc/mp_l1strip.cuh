@@ -302,7 +302,7 @@ cudaError_t launch_reg_nt(const RegGeom& g, const T* y, T* x, int64_t n, int64_t
           if (l1_tma_enabled() && reinterpret_cast<uintptr_t>(y) % 16 == 0 &&
               reinterpret_cast<uintptr_t>(x) % 16 == 0 && encode_strip_map<T>(&maps.y, y, n, m) &&
               encode_strip_map<T>(&maps.x, x, n, m))
-            return launch_reg<T, 2, 256, kRegTmaRS, true>(y, x, n, m, v, u, ws, info, dv, s, &maps);
+            return launch_reg<T, 2, 256, tma_rs(256), true>(y, x, n, m, v, u, ws, info, dv, s, &maps);
         }
         return launch_reg<T, 2, 256, kRegHybridRS>(y, x, n, m, v, u, ws, info, dv, s);
       }
@@ -311,7 +311,7 @@ cudaError_t launch_reg_nt(const RegGeom& g, const T* y, T* x, int64_t n, int64_t
         if (l1_tma_enabled() && reinterpret_cast<uintptr_t>(y) % 16 == 0 &&
             reinterpret_cast<uintptr_t>(x) % 16 == 0 && encode_strip_map<T>(&maps.y, y, n, m) &&
             encode_strip_map<T>(&maps.x, x, n, m))
-          return launch_reg<T, 2, kRegThreads, kRegTmaRS, true>(y, x, n, m, v, u, ws, info, dv, s, &maps);
+          return launch_reg<T, 2, kRegThreads, tma_rs(kRegThreads), true>(y, x, n, m, v, u, ws, info, dv, s, &maps);
       }
       return launch_reg<T, 2, kRegThreads, kRegHybridRS>(y, x, n, m, v, u, ws, info, dv, s);
     }
@@ -384,7 +384,7 @@ cudaError_t launch_l1strip(const T* y, T* x, int64_t n, int64_t m, const double*
         reinterpret_cast<uintptr_t>(y) % 16 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0) {
       TmaMaps maps{};
       if (encode_strip_map<T>(&maps.y, y, n, m) && encode_strip_map<T>(&maps.x, x, n, m))
-        return launch_reg<T, 2, 128, kRegTmaRS, true>(y, x, n, m, v, u, ws, info, dv, s, &maps);
+        return launch_reg<T, 2, 128, tma_rs(128), true>(y, x, n, m, v, u, ws, info, dv, s, &maps);
     }
     switch (g.P) {
       case 8: return launch_reg_nt<T, 8>(g, y, x, n, m, v, u, ws, info, dv, s);
