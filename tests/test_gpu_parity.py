@@ -221,12 +221,14 @@ def test_large_vector_ball():
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
 @pytest.mark.parametrize("n,m", [(1000, 64), (2000, 48), (4096, 24), (8000, 12), (8193, 8), (3000, 6), (1, 32),
-                                 (7, 4), (4095, 40)])
+                                 (7, 4), (4095, 40), (513, 24), (1025, 32), (2049, 16), (4097, 8)])
 def test_l11_register_and_staged_geometries(dt, n, m):
     """Every K3b l1 route: register strips of 16P-byte row pieces (P = 8, 4,
-    2, 1 by n), the shared-memory quad strip (n > 8192) and the column
-    kernels (m not a multiple of 4); mixed column scales so strips hold
-    zeroed, projected and (p = 2) shrunk columns; tie-heavy integer data."""
+    2, 1 by n), the TMA strips at their row-count boundaries (128 threads:
+    513 / 1025..2048 rows; 256: 2049..4096; f64 512: 4097..8192), the
+    shared-memory quad strip (n > 8192) and the column kernels (m not a
+    multiple of 4); mixed column scales so strips hold zeroed, projected and
+    (p = 2) shrunk columns; tie-heavy integer data."""
     rng = np.random.default_rng(n * 7 + m)
     scale = np.exp(rng.normal(size=m) * 1.5)
     for kind in ("normal", "ties"):
