@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 import subprocess
 
 import numpy as np
@@ -50,8 +51,8 @@ def build(ref: bool | None = None) -> None:
     if ref is None:
         ref = os.path.isdir("/root/reference/proj/src")
     if ref:
-        targets.append("ref")
-    subprocess.run(["make", "-s", "-j8", "-C", HERE] + targets, check=True)
+        targets += ["ref", "suites"]
+    subprocess.run(["make", "-s", "-j8", "-C", HERE, f"PYTHON={sys.executable}"] + targets, check=True)
 
 
 _lib = None

@@ -35,8 +35,13 @@ def _is_torch(a) -> bool:
     return type(a).__module__.startswith("torch")
 
 
+def _is_cuda_tensor(a) -> bool:
+    """torch CUDA tensors take the device path; CPU tensors are host arrays."""
+    return _is_torch(a) and a.device.type == "cuda"
+
+
 def _host_array(a) -> np.ndarray:
-    arr = np.asarray(a)
+    arr = a.detach().numpy() if _is_torch(a) else np.asarray(a)
     if arr.dtype != np.float32:
         arr = arr.astype(np.float64)
     return np.ascontiguousarray(arr)
@@ -53,11 +58,48 @@ def _dt(arr) -> int:
     return MP_F32 if arr.dtype == np.float32 else MP_F64
 
 
+def _torch_dtype(dtype):
+    """Strict dtype map for the device projectors: float32 / float64 only.
+
+    Anything else (float16, bfloat16, integers) would have the kernels read
+    and write 8-byte elements through a 2- or 4-byte buffer, so it raises."""
+    import torch
+    if dtype in (torch.float32, "float32", "torch.float32", np.float32):
+        return torch.float32, MP_F32
+    if dtype in (torch.float64, "float64", "torch.float64", np.float64):
+        return torch.float64, MP_F64
+    raise MpConfigError(f"unsupported dtype {dtype}: the projections compute in float32 or float64")
+
+
+def _check_operand(t, name, shape, tdtype, device):
+    import torch
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+        raise MpConfigError(f"{name} must be a CUDA tensor")
+    if t.device != device:
+        raise MpConfigError(f"{name} is on {t.device}, the projector was planned for {device}")
+    if t.dtype != tdtype:
+        raise MpConfigError(f"{name} has dtype {t.dtype}, the projector was planned for {tdtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise MpShapeError(f"{name} has shape {tuple(t.shape)}, the projector was planned for {tuple(shape)}")
+    if not t.is_contiguous():
+        raise MpConfigError(f"{name} must be contiguous (row-major fibers)")
+
+
 def _ptr(a) -> int:
     return a.data_ptr() if _is_torch(a) else a.ctypes.data
 
 
 # -------------------------------------------------------------- device path
+def _cuda_device(device):
+    import torch
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    d = torch.device(device)
+    if d.type != "cuda":
+        raise MpConfigError(f"device projectors run on CUDA devices, not {d}")
+    return torch.device("cuda", d.index if d.index is not None else torch.cuda.current_device())
+
+
 class BilevelProjector:
     """Pre-planned bi-level projection on device tensors.
 
@@ -67,11 +109,10 @@ class BilevelProjector:
     def __init__(self, n: int, m: int, dtype="float32", p="1", q="inf", device=None, flags: int = 0):
         import torch
         self.n, self.m = int(n), int(m)
-        self.tdtype = torch.float32 if str(dtype) in ("float32", "torch.float32") else torch.float64
-        self.dt = MP_F32 if self.tdtype == torch.float32 else MP_F64
+        self.tdtype, self.dt = _torch_dtype(dtype)
         self.p, self.q = norm_code(p), norm_code(q)
         self.flags = flags
-        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device = _cuda_device(device)
         wsb = lib().mp_bilevel_workspace_size(self.dt, self.n, self.m, self.p, self.q)
         if wsb == 0:
             raise MpShapeError("bilevel_project requires a non-empty order-2 tensor")
@@ -82,6 +123,8 @@ class BilevelProjector:
 
     def __call__(self, y, x, eta: float, stream=None):
         import torch
+        _check_operand(y, "y", (self.n, self.m), self.tdtype, self.device)
+        _check_operand(x, "x", (self.n, self.m), self.tdtype, self.device)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         check(lib().mp_bilevel_project(y.data_ptr(), x.data_ptr(), self.dt, self.n, self.m, self.p, self.q,
                                        float(eta), self.budgets.data_ptr(), self.norms.data_ptr(),
@@ -102,10 +145,9 @@ class MultilevelProjector:
         self.want_chain = want_chain  # False lets (inf, ..., inf, p) specs collapse to one bi-level pass
         self.shape = [int(s) for s in shape]
         self.levels = parse_norm_spec(levels)
-        self.tdtype = torch.float32 if str(dtype) in ("float32", "torch.float32") else torch.float64
-        self.dt = MP_F32 if self.tdtype == torch.float32 else MP_F64
+        self.tdtype, self.dt = _torch_dtype(dtype)
         self.flags = flags
-        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device = _cuda_device(device)
         self._shape_c = (C.c_int64 * len(self.shape))(*self.shape)
         self._lv_c = (C.c_int * max(1, len(self.levels)))(*self.levels)
         wsb = lib().mp_multilevel_workspace_size(self.dt, self._shape_c, len(self.shape), self._lv_c,
@@ -123,6 +165,8 @@ class MultilevelProjector:
 
     def __call__(self, t, x, eta: float, stream=None):
         import torch
+        _check_operand(t, "t", self.shape, self.tdtype, self.device)
+        _check_operand(x, "x", self.shape, self.tdtype, self.device)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         check(lib().mp_multilevel_project(t.data_ptr(), x.data_ptr(), self.dt, self._shape_c, len(self.shape),
                                           self._lv_c, len(self.levels), float(eta),
@@ -152,7 +196,7 @@ def bilevel_project(y, eta, p="1", q="inf", workers=1, flags: int = 0):
     compatibility; the CUDA grid replaces the CPU pool."""
     del workers
     pc, qc = norm_code(p), norm_code(q)
-    if _is_torch(y):
+    if _is_cuda_tensor(y):
         if y.dim() != 2:
             raise MpShapeError("bilevel_project requires order 2")
         yc = y.contiguous()
@@ -199,7 +243,7 @@ def multilevel_project(y, norms, eta, workers=1, flags: int = 0, return_chain: b
     -> multilevel_project_iter, proj/src/multilevel.cpp:93-124)."""
     del workers
     levels = parse_norm_spec(norms)
-    if _is_torch(y):
+    if _is_cuda_tensor(y):
         t = y.contiguous()
         proj = MultilevelProjector(t.shape, levels, t.dtype, t.device, flags)
         x = proj(t, t.clone(), eta)
@@ -315,7 +359,7 @@ def euclid_project_l1inf(y, eta):
 
     Mirrors ``multiproj.euclid_project_l1inf`` (proj/python/bindings.cpp:101-108
     -> proj/src/euclidean.cpp:82-170)."""
-    if _is_torch(y):
+    if _is_cuda_tensor(y):
         import torch
         if y.dim() != 2:
             raise MpShapeError("euclid_project_l1inf requires order 2")
@@ -349,6 +393,8 @@ def perturb_gaussian(x, sigma, seed, iteration, stream=None):
     """In-place x += sigma * N(0,1) on a torch CUDA tensor (config-5 loop
     harness; Philox4x32-10 keyed by (seed, iteration))."""
     import torch
+    if not _is_cuda_tensor(x) or not x.is_contiguous():
+        raise MpConfigError("perturb_gaussian needs a contiguous CUDA tensor")
     s = stream if stream is not None else torch.cuda.current_stream(x.device)
     check(lib().mp_perturb_gaussian(x.data_ptr(), _dt(x), x.numel(), float(sigma), int(seed), int(iteration),
                                     s.cuda_stream))

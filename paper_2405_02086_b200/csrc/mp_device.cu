@@ -275,14 +275,13 @@ cudaError_t outer_attr() {
 }
 
 cudaError_t outer_setup() {
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [] {
+  static std::atomic<uint64_t> done{0};
+  return mpi::once_per_device(done, [] {
     for (cudaError_t e : {outer_attr<1>(), outer_attr<2>(), outer_attr<4>(), outer_attr<8>(), outer_attr<12>(),
                           outer_attr<16>(), outer_attr<24>(), mpk::l1strip_setup()})
-      if (e != cudaSuccess && err == cudaSuccess) err = e;
+      if (e != cudaSuccess) return e;
+    return cudaSuccess;
   });
-  return err;
 }
 
 // K2 on a cluster of C CTAs (PDL + cluster launch attributes).
@@ -762,9 +761,11 @@ bool euclid_fits(int64_t n) {
 template <typename T, int E>
 cudaError_t launch_eu_sort(T* mags, mpk::DD* pref, int64_t n, int64_t m, int P2, int nt, size_t smem,
                            const mp_info* inf, cudaStream_t s) {
-  static const cudaError_t attr = cudaFuncSetAttribute(mpk::k_eu_sort<T, E>,
-                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       static_cast<int>(mpk::kEuSortSmemMax));
+  static std::atomic<uint64_t> done{0};
+  const cudaError_t attr = mpi::once_per_device(done, [] {
+    return cudaFuncSetAttribute(mpk::k_eu_sort<T, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(mpk::kEuSortSmemMax));
+  });
   if (attr != cudaSuccess) return attr;
   mpk::k_eu_sort<T, E><<<static_cast<unsigned>(m), nt, smem, s>>>(mags, pref, n, P2, inf);
   return cudaGetLastError();
@@ -775,9 +776,11 @@ template <typename T, int NT>
 cudaError_t launch_eu_radix(T* mags, mpk::DD* pref, int64_t n, int64_t m, const mp_info* inf, cudaStream_t s) {
   using Sort = cub::BlockRadixSort<typename mpk::BitsT<T>::type, NT, 16, cub::NullType, mpk::kEuRadixBits>;
   constexpr size_t smem = sizeof(typename Sort::TempStorage);
-  static const cudaError_t attr = cudaFuncSetAttribute(mpk::k_eu_sort_radix<T, NT, 16>,
-                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       static_cast<int>(smem));
+  static std::atomic<uint64_t> done{0};
+  const cudaError_t attr = mpi::once_per_device(done, [] {
+    return cudaFuncSetAttribute(mpk::k_eu_sort_radix<T, NT, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem));
+  });
   if (attr != cudaSuccess) return attr;
   mpk::k_eu_sort_radix<T, NT, 16><<<static_cast<unsigned>(m), NT, smem, s>>>(mags, pref, n, inf);
   return cudaGetLastError();
@@ -803,7 +806,7 @@ mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, doubl
   // radix-sorted columns (cub::BlockRadixSort, 16 keys per thread) for
   // 1024 <= P2 <= 16384; MP_EU_SORT=bitonic keeps the network (A/B aid)
   static const bool bitonic_only = [] {
-    const char* e = std::getenv("MP_EU_SORT");
+    const char* e = mpk::mp_tuning_env("MP_EU_SORT");
     return e && std::strcmp(e, "bitonic") == 0;
   }();
   if (!bitonic_only && ek == 16 && nt >= 64 && nt <= 1024) {

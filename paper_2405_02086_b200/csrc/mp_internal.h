@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdarg>
 #include <cstddef>
 #include <cstdint>
@@ -53,5 +54,20 @@ inline bool norm_ok(int q) { return q == MP_NORM_L1 || q == MP_NORM_L2 || q == M
 inline bool dtype_ok(int d) { return d == MP_F32 || d == MP_F64; }
 
 int sm_count();
+
+// Function attributes (dynamic shared memory limits, non-portable cluster
+// sizes) belong to a device context.  Bit d of `done` marks device d as set
+// up; f() must be idempotent (two threads may both run it for one device).
+template <class F>
+cudaError_t once_per_device(std::atomic<uint64_t>& done, F&& f) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (dev < 64 && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  e = f();
+  if (e == cudaSuccess && dev < 64) done.fetch_or(bit, std::memory_order_release);
+  return e;
+}
 
 }  // namespace mpi

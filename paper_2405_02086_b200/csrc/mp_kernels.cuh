@@ -10,10 +10,12 @@
 //                      (deterministic, run-to-run bit-reproducible).
 //   K2 k_outer         the outer projection of the norm vector
 //                      (proj/src/vector_balls.cpp:150-191,207-214) entirely on
-//                      device: one CTA, vector in shared memory, f64 Michelot
-//                      fixed point for the l1 threshold, final tau from a
-//                      double-double sum over {v >= cutoff} (the reference sums
-//                      in long double, vector_balls.cpp:32-40).
+//                      device: one register CTA, a <=16-CTA DSMEM cluster or a
+//                      cooperative grid; f64 Michelot fixed point for the l1
+//                      threshold, tau = (sum_A v - eta)/|A| from fixed-order
+//                      f64 tree sums over the final active set A (the
+//                      reference sums in long double, vector_balls.cpp:32-40;
+//                      agreement ~1e-15 relative).
 //   K3 k_apply         fused clamp / scale (proj/src/fiber_kernels.cpp:37-55),
 //                      streaming loads/stores, zero-budget column groups
 //                      written without being read, row blocks swept in reverse
@@ -418,9 +420,6 @@ __device__ __forceinline__ long long block_count(long long c, long long* scr) {
   __syncthreads();
   c = (lane < (blockDim.x >> 5)) ? scr[lane] : 0;
   return warp_reduce(c, [](long long a, long long b) { return a + b; });
-}
-__device__ __forceinline__ int block_or(int v, int* scr) {
-  return __syncthreads_or(v);
 }
 
 // ------------------------------------------------------------------- K2

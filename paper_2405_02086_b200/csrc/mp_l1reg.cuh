@@ -26,9 +26,9 @@
 // Passes come in two kinds.  FAST (f32 strips, far from convergence): f32
 // per-thread sums (an f32->f64 convert per element would cost more than the
 // pass), f64 across threads, and a step to a rigorous LOWER bound of the
-// exact iterate: a thread partial sums <= RPT nonnegative f32 terms, so
-// S >= S_exact (1 - RPT 2^-24) and S_lo = S (1 - 2^-17), rounded down, is
-// below S_exact; t' = RD((S_lo - RU(u_j)) / K) <= (S_exact - u_j) / K.
+// exact iterate: a thread partial sums NPC <= 32 nonnegative f32 terms, the
+// warp and CTA totals add 5 + NW more, so S >= S_exact (1 - 53 2^-24) and
+// S_lo = S (1 - 2^-17), rounded down, is below S_exact; t' = RD((S_lo - RU(u_j)) / K) <= (S_exact - u_j) / K.
 // Michelot from below stays below tau and the set only shrinks (f64 strips:
 // f64 sums, the step nudged 2^-45 below).  EXACT (near convergence -- the
 // count dropped by < 1/16): f64 sums, plus min |y| over the set.  With t_ex = (S - u_j) / K,
@@ -267,7 +267,13 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
   land_smem(strip);
   pdl_wait();
   tl_begin(3);
-  if (info->status != MP_OK) return;
+  if (info->status != MP_OK) {
+    // drain the copies already aimed at this CTA's shared memory before it
+    // is released (another resident CTA may reuse it)
+    if constexpr (TMA) mbar_wait(&mbar, mph);
+    else if constexpr (RS > 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
+    return;
+  }
 
   auto piece = [&](int i) -> uint4 {  // i is a compile-time index after unrolling
     if (RS == 0 || i < RPT) return q[i < RPT ? i : 0];
@@ -381,7 +387,7 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
 #pragma unroll
             for (int w = 1; w < NW; ++w) tot = rp_add(tot, wx[par][w][lane]);
           } else {
-            AccT s32 = AccT(0);  // f32: <= RPT + 5 + NW f32 terms per sum
+            AccT s32 = AccT(0);  // f32: <= NPC + 5 + NW f32 terms per sum
             float k32 = 0.0f;
 #pragma unroll
             for (int w = 0; w < NW; ++w) {
@@ -405,7 +411,8 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
           } else {
             if constexpr (kF32) {
               // a rigorous lower bound of (S_exact - u_j) / K: the f32 sums
-              // carry < 40 * 2^-24 relative error, the margin is 2^-17
+              // carry < (NPC + 5 + NW) * 2^-24 <= 53 * 2^-24 relative error,
+              // the margin is 2^-17
               const float xs = __fsub_rd(__fmul_rd(__double2float_rd(tot.s), 1.0f - 0x1p-17f), uup);
               const float tn = xs > 0.0f ? __fmul_rd(xs, __frcp_rd(static_cast<float>(tot.k))) : 0.0f;
               td = fmax(td, static_cast<double>(tn));
@@ -493,10 +500,13 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
       if (need_store) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
       if (tid == 0) {
-        // four store groups: each quarter's boxes reload as soon as the
-        // engine has read them, while the later quarters are still being
-        // read (one group: 179 us on config 3, two or four: 173 us)
-        constexpr int kQ = kBoxes / 4;  // groups [0,kQ) [kQ,2kQ) [2kQ,3kQ) [3kQ,kBoxes)
+        // up to four store groups: each group's boxes reload as soon as the
+        // engine has read them, while the later groups are still being read
+        // (one group: 179 us on config 3, two or four: 173 us).  Group g is
+        // boxes [g * kBoxes / kG, (g + 1) * kBoxes / kG); 64-thread strips
+        // have three boxes, hence three groups.
+        constexpr int kG = kBoxes < 4 ? kBoxes : 4;
+        static_assert(kG >= 1, "TMA strips: at least one box");
         auto store = [&](int b0, int b1) {
           for (int b = b0; b < b1; ++b)
             tma_store_2d(&tm.x, static_cast<int>(strip * W), SL * RPT + b * kBoxRows,
@@ -509,20 +519,21 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
                         static_cast<int>(next * W), SL * RPT + b * kBoxRows, &mbar);
         };
         if (need_store) {
-          store(0, kQ);
-          store(kQ, 2 * kQ);
-          store(2 * kQ, 3 * kQ);
-          store(3 * kQ, kBoxes);
+#pragma unroll
+          for (int g = 0; g < kG; ++g) store(g * kBoxes / kG, (g + 1) * kBoxes / kG);
         }
         if (more) mbar_expect(&mbar, static_cast<unsigned>(RS * NT * 16));
-        if (need_store) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
-        if (more) load(0, kQ);
-        if (need_store) asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
-        if (more) load(kQ, 2 * kQ);
-        if (need_store) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        if (more) load(2 * kQ, 3 * kQ);
-        if (need_store) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        if (more) load(3 * kQ, kBoxes);
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+          // groups still allowed in flight: kG - 1 - g (wait_group takes an immediate)
+          if (need_store) {
+            if (kG - 1 - g == 3) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+            else if (kG - 1 - g == 2) asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
+            else if (kG - 1 - g == 1) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
+          if (more) load(g * kBoxes / kG, (g + 1) * kBoxes / kG);
+        }
       }
     } else if constexpr (RS > 0) {
       if (more) {

@@ -200,10 +200,18 @@ struct L1Derive {
   mp_info* info_w = nullptr;
 };
 
+// Route switches for A/B timing.  The product build compiles them to their
+// defaults; only a build with -DMP_TUNING_SWITCHES reads the environment.
+#ifdef MP_TUNING_SWITCHES
+inline const char* mp_tuning_env(const char* name) { return std::getenv(name); }
+#else
+inline const char* mp_tuning_env(const char*) { return nullptr; }
+#endif
+
 // MP_L1_KERNEL=quad forces the shared-memory path (A/B timing aid).
 inline bool l1reg_disabled() {
   static const bool d = [] {
-    const char* e = std::getenv("MP_L1_KERNEL");
+    const char* e = mp_tuning_env("MP_L1_KERNEL");
     return e && std::strcmp(e, "quad") == 0;
   }();
   return d;
@@ -212,7 +220,7 @@ inline bool l1reg_disabled() {
 // MP_L1REG_P=1|2|4|8 caps the register path's pieces per row (tuning aid).
 inline int l1reg_prefer_p() {
   static const int p = [] {
-    const char* e = std::getenv("MP_L1REG_P");
+    const char* e = mp_tuning_env("MP_L1REG_P");
     return e ? std::atoi(e) : 0;
   }();
   return p;
@@ -224,7 +232,7 @@ inline int l1reg_prefer_p() {
 // cp.async / LSU path (A/B aid).
 inline bool l1_tma_enabled() {
   static const bool on = [] {
-    const char* e = std::getenv("MP_L1_TMA");
+    const char* e = mp_tuning_env("MP_L1_TMA");
     return !(e && *e == '0');
   }();
   return on;
@@ -262,12 +270,15 @@ cudaError_t launch_reg(const T* y, T* x, int64_t n, int64_t m, const double* v, 
   const int64_t nstrips = m / W;
   const size_t smem = static_cast<size_t>(NT) * RS * 16;
   if constexpr (RS > 0) {
-    static const cudaError_t a1 = cudaFuncSetAttribute(k_l1reg<T, P, true, true, NT, RS, TMA>,
-                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    static const cudaError_t a2 = cudaFuncSetAttribute(k_l1reg<T, P, false, true, NT, RS, TMA>,
-                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (a1 != cudaSuccess) return a1;
-    if (a2 != cudaSuccess) return a2;
+    static std::atomic<uint64_t> done{0};
+    const cudaError_t a = mpi::once_per_device(done, [smem] {
+      const cudaError_t a1 = cudaFuncSetAttribute(k_l1reg<T, P, true, true, NT, RS, TMA>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (a1 != cudaSuccess) return a1;
+      return cudaFuncSetAttribute(k_l1reg<T, P, false, true, NT, RS, TMA>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    if (a != cudaSuccess) return a;
   }
   TmaMaps tm{};
   if (maps) tm = *maps;

@@ -19,6 +19,12 @@ projection of the whole matrix: bit for bit for l_inf column maxima (exact),
 to f64 rounding of the column sums for l1 / l2 (their row grouping follows
 the grid, which depends on the block width).
 
+``ShardedBilevelProjector`` plans once (the only host sync: one all-gather of
+the block widths) and then projects with no host synchronisation, no
+allocation in the C-ABI calls and exactly one collective per call
+(``all_gather_into_tensor`` of the fixed-width padded norm blocks), so a call
+can sit inside a captured CUDA graph next to the training step.
+
 The local compute is a pluggable backend: ``CudaBackend`` drives the sm_100a
 kernels through the C-ABI (the product path).  Tests may pass a CPU backend
 built on the oracle to exercise the sharding logic with gloo on CPU.
@@ -34,94 +40,143 @@ from . import _capi
 
 class CudaBackend:
     """Local steps on torch CUDA tensors through the C-ABI (mp_aggregate,
-    mp_project_ball, mp_project_fibers)."""
+    mp_project_ball, mp_project_fibers).  ``plan`` sizes every workspace once;
+    the per-call methods write into caller-provided outputs and never sync."""
 
     def __init__(self, device=None):
         import torch
         self.torch = torch
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.lib = _capi.lib()
+        self.ws = None
 
-    def _ws(self, nbytes):
-        return self.torch.empty(max(int(nbytes), 256), dtype=self.torch.uint8, device=self.device)
+    def plan(self, n: int, m_local: int, m: int, dt: int, p: int, q: int):
+        t, L = self.torch, self.lib
+        need = max(L.mp_aggregate_workspace_size(dt, n, m_local, q),
+                   L.mp_project_ball_workspace_size(_capi.MP_F64, m, p),
+                   L.mp_project_fibers_workspace_size(dt, n, m_local, q), 256)
+        self.ws = t.empty(int(need), dtype=t.uint8, device=self.device)
+        self.info = t.zeros(C.sizeof(_capi.MpInfo), dtype=t.uint8, device=self.device)
 
-    def norms(self, y_local, q: int):
-        t = self.torch
+    def _stream(self):
+        return self.torch.cuda.current_stream(self.device).cuda_stream
+
+    def norms(self, y_local, q: int, out):
         n, m = y_local.shape
-        dt = _capi.MP_F32 if y_local.dtype == t.float32 else _capi.MP_F64
-        out = t.empty(m, dtype=t.float64, device=self.device)
-        ws = self._ws(self.lib.mp_aggregate_workspace_size(dt, n, m, q))
-        s = t.cuda.current_stream(self.device)
-        _capi.check(self.lib.mp_aggregate(y_local.data_ptr(), out.data_ptr(), dt, n, m, q, ws.data_ptr(), ws.numel(),
-                                          s.cuda_stream))
+        _capi.check(self.lib.mp_aggregate(y_local.data_ptr(), out.data_ptr(), _dtype_code(y_local), n, m, q,
+                                          self.ws.data_ptr(), self.ws.numel(), self._stream()))
         return out
 
-    def outer(self, v, p: int, eta: float):
-        t = self.torch
-        u = t.empty_like(v)
-        ws = self._ws(self.lib.mp_project_ball_workspace_size(_capi.MP_F64, v.numel(), p))
-        info = t.zeros(C.sizeof(_capi.MpInfo), dtype=t.uint8, device=self.device)
-        s = t.cuda.current_stream(self.device)
-        _capi.check(self.lib.mp_project_ball(v.data_ptr(), u.data_ptr(), _capi.MP_F64, v.numel(), p, float(eta),
-                                             info.data_ptr(), ws.data_ptr(), ws.numel(), s.cuda_stream))
-        st = _capi.MpInfo.from_buffer_copy(info.cpu().numpy().tobytes()).status
-        _capi.check(st)
-        return u
+    def outer(self, v, p: int, eta: float, out):
+        _capi.check(self.lib.mp_project_ball(v.data_ptr(), out.data_ptr(), _capi.MP_F64, v.numel(), p, float(eta),
+                                             self.info.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                                             self._stream()))
+        return out
 
     def apply(self, y_local, x_local, q: int, v_local, u_local, flags: int = 0):
-        t = self.torch
         n, m = y_local.shape
-        dt = _capi.MP_F32 if y_local.dtype == t.float32 else _capi.MP_F64
-        ws = self._ws(self.lib.mp_project_fibers_workspace_size(dt, n, m, q))
-        s = t.cuda.current_stream(self.device)
-        _capi.check(self.lib.mp_project_fibers(y_local.data_ptr(), x_local.data_ptr(), dt, n, m, q,
-                                               v_local.contiguous().data_ptr(), u_local.contiguous().data_ptr(),
-                                               flags, ws.data_ptr(), ws.numel(), s.cuda_stream))
+        _capi.check(self.lib.mp_project_fibers(y_local.data_ptr(), x_local.data_ptr(), _dtype_code(y_local), n, m,
+                                               q, v_local.data_ptr(), u_local.data_ptr(), flags,
+                                               self.ws.data_ptr(), self.ws.numel(), self._stream()))
         return x_local
 
-    def gather(self, v_local, group=None):
-        return gather_norms(v_local, group)
+    def status(self) -> int:
+        """Device status of the last outer projection (syncs)."""
+        return _capi.MpInfo.from_buffer_copy(self.info.cpu().numpy().tobytes()).status
 
 
-def gather_norms(v_local, group=None):
-    """All-gather variable-length norm vectors (torch tensors) in rank order."""
+def _dtype_code(t) -> int:
     import torch
-    import torch.distributed as td
-    world = td.get_world_size(group)
-    dev = v_local.device
-    sizes = torch.tensor([v_local.numel()], dtype=torch.int64, device=dev)
-    all_sizes = [torch.zeros_like(sizes) for _ in range(world)]
-    td.all_gather(all_sizes, sizes, group=group)
-    mx = int(max(int(s.item()) for s in all_sizes))
-    pad = torch.zeros(mx, dtype=v_local.dtype, device=dev)
-    pad[:v_local.numel()] = v_local
-    parts = [torch.empty_like(pad) for _ in range(world)]
-    td.all_gather(parts, pad, group=group)
-    return torch.cat([parts[r][:int(all_sizes[r].item())] for r in range(world)])
+    if t.dtype == torch.float32:
+        return _capi.MP_F32
+    if t.dtype == torch.float64:
+        return _capi.MP_F64
+    raise _capi.MpConfigError(f"unsupported dtype {t.dtype}")
+
+
+class ShardedBilevelProjector:
+    """Planned column-sharded bi-level projection; every rank of ``group``
+    constructs one and calls it collectively.
+
+    ``__call__(y_local, x_local, eta)`` writes this rank's projected block
+    into x_local (may be y_local).  Per call: local K1, one
+    ``all_gather_into_tensor`` of the norm blocks padded to the widest block,
+    the outer projection on every rank, the local apply, and an on-device
+    zero-column count -- no host sync, nothing allocated by the C-ABI."""
+
+    def __init__(self, n: int, m_local: int, dtype, p="1", q="inf", group=None, backend=None, flags: int = 0,
+                 device=None):
+        import torch
+        import torch.distributed as td
+        self.group, self.flags = group, flags
+        self.pc, self.qc = _capi.norm_code(p), _capi.norm_code(q)
+        self.n, self.m_local = int(n), int(m_local)
+        self.world, self.rank = td.get_world_size(group), td.get_rank(group)
+        self.be = backend or CudaBackend(device)
+        dev = getattr(self.be, "device", torch.device("cpu"))
+        # plan-time exchange of block widths (the only host sync)
+        mine = torch.tensor([self.m_local], dtype=torch.int64, device=dev)
+        widths = torch.empty(self.world, dtype=torch.int64, device=dev)
+        td.all_gather_into_tensor(widths, mine, group=group)
+        self.widths = [int(w) for w in widths.cpu().tolist()]
+        self.c0 = sum(self.widths[:self.rank])
+        self.m = sum(self.widths)
+        self.pad = max(self.widths)
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.send = torch.zeros(self.pad, **f64)
+        self.recv = torch.empty(self.world * self.pad, **f64)
+        if all(w == self.pad for w in self.widths):
+            self.index = None
+            self.v = self.recv
+        else:
+            idx = [r * self.pad + k for r, w in enumerate(self.widths) for k in range(w)]
+            self.index = torch.tensor(idx, dtype=torch.int64, device=dev)
+            self.v = torch.empty(self.m, **f64)
+        self.u = torch.empty(self.m, **f64)
+        self.zero_count = torch.zeros((), dtype=torch.int64, device=dev)
+        dt = _dtype_code(torch.empty(0, dtype=dtype))
+        if hasattr(self.be, "plan"):
+            self.be.plan(self.n, self.m_local, self.m, dt, self.pc, self.qc)
+
+    def __call__(self, y_local, x_local, eta: float):
+        import torch
+        import torch.distributed as td
+        if not (eta >= 0.0) or not np.isfinite(eta):
+            raise _capi.MpValueError("radius must be a finite nonnegative real")
+        if tuple(y_local.shape) != (self.n, self.m_local):
+            raise _capi.MpShapeError(f"planned for a ({self.n}, {self.m_local}) block, got {tuple(y_local.shape)}")
+        v_local = self.send[:self.m_local]
+        self.be.norms(y_local, self.qc, v_local)
+        td.all_gather_into_tensor(self.recv, self.send, group=self.group)
+        if self.index is not None:
+            torch.index_select(self.recv, 0, self.index, out=self.v)
+        self.be.outer(self.v, self.pc, eta, self.u)
+        self.be.apply(y_local, x_local, self.qc, v_local, self.budgets, self.flags)
+        torch.sum((self.u == 0) | (self.v == 0), dim=0, out=self.zero_count)
+        return x_local
+
+    @property
+    def budgets(self):
+        """This rank's slice of the budgets u (device tensor, no copy)."""
+        return self.u[self.c0:self.c0 + self.m_local]
+
+    def zero_columns(self) -> int:
+        """Global zeroed-column count of the last call (syncs; raises the
+        outer projection's device status if it failed)."""
+        if hasattr(self.be, "status"):
+            _capi.check(self.be.status())
+        return int(self.zero_count.item())
 
 
 def sharded_bilevel_project(y_local, eta: float, p="1", q="inf", backend=None, group=None, flags: int = 0):
-    """Project the global matrix whose column block this rank holds.
+    """One-shot form: plan, project, and read the zero count.
 
     Returns (x_local, budgets_local, zero_columns_global).  Every rank must
     call it (collective); blocks are concatenated in rank order."""
-    import torch.distributed as td
-    pc, qc = _capi.norm_code(p), _capi.norm_code(q)
     if not (eta >= 0.0) or not np.isfinite(eta):
         raise _capi.MpValueError("radius must be a finite nonnegative real")
-    be = backend or CudaBackend(getattr(y_local, "device", None))
-    rank = td.get_rank(group)
-    v_local = be.norms(y_local, qc)
-    v = be.gather(v_local, group)
-    # offsets of this rank's block in the gathered vector
-    import torch
-    world = td.get_world_size(group)
-    counts = torch.tensor([v_local.numel()], dtype=torch.int64, device=v_local.device)
-    all_counts = [torch.zeros_like(counts) for _ in range(world)]
-    td.all_gather(all_counts, counts, group=group)
-    c0 = int(sum(int(c.item()) for c in all_counts[:rank]))
-    u = be.outer(v, pc, eta)
-    u_local = u[c0:c0 + v_local.numel()]
-    x_local = be.apply(y_local, y_local.clone(), qc, v_local, u_local, flags)
-    zero_columns = int(((u == 0) | (v == 0)).sum().item())
-    return x_local, u_local, zero_columns
+    n, m_local = y_local.shape
+    proj = ShardedBilevelProjector(n, m_local, y_local.dtype, p, q, group=group, backend=backend, flags=flags,
+                                   device=getattr(y_local, "device", None))
+    x_local = proj(y_local, y_local.clone(), eta)
+    return x_local, proj.budgets.clone(), proj.zero_columns()

@@ -22,9 +22,9 @@ from . import BilevelProjector
 
 class FeatureProjector:
     """``hook()`` projects ``weight`` in place onto {W : sum_f ||W_f||_q <= eta}
-    (outer l1 over the feature groups f, inner q-norm within a group) and
-    returns the number of zeroed feature groups from the last call (device
-    sync; ``zero_features(sync=False)`` skips it)."""
+    (outer l1 over the feature groups f, inner q-norm within a group) without
+    a host sync; ``zero_features()`` reads the number of zeroed feature groups
+    of the last call (that read syncs)."""
 
     def __init__(self, weight, eta: float, q="inf", feature_dim: int = 1, flags: int = 0):
         import torch

@@ -60,3 +60,72 @@ def check_bilevel(x_gpu, y, ref: dict, q: str, tau_gpu: float | None = None, rto
     rel = err / np.maximum(np.abs(x_ref), 1e-300)
     return {"max_rel": float(rel[x_ref != 0].max()) if np.any(x_ref != 0) else 0.0,
             "near": int(near.sum()), "zero_columns": int(zr.sum())}
+
+
+def _l1_fiber_taus(v: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """Per-fiber l1 thresholds (fibers along axis 0) recovered from norms v and
+    projected budgets u: every positive u equals v - tau."""
+    d = np.where(u > 0.0, v - u, -np.inf)
+    return d.max(axis=0) if d.ndim > 1 else np.asarray(d.max())
+
+
+def _near_slack(v: np.ndarray, u: np.ndarray, rtol: float) -> np.ndarray:
+    """tau_f where an entry's norm is within rtol * tau_f of its fiber's l1
+    threshold (its budget may be 0 or up to rtol * tau_f), else 0."""
+    tau = _l1_fiber_taus(v, u)
+    has = np.isfinite(tau) & (tau > 0)
+    tau = np.where(has, tau, 0.0)
+    return np.where(has & (np.abs(v - tau) <= rtol * tau), tau, 0.0) * np.ones_like(v)
+
+
+def check_multilevel(x_gpu, t, levels, x_ref, chain_ref, chain_gpu=None, rtol: float = 1e-5) -> dict:
+    """§8(c) rule applied per level of a multi-level projection.
+
+    levels are innermost first (codes 0 = l1, 1 = l2, 2 = inf); chain_ref /
+    chain_gpu are budget chains deepest first (U_{r-1}, ..., U_1).  Each budget
+    U_k may differ by rtol * (|U_k| + S_k); S_k is the near-threshold slack: an
+    entry whose norm lies within rtol * tau of its fiber's l1 threshold tau
+    carries tau, and a fiber inherits its parent's slack (the l1 / l2 / inf
+    projections move a child budget by at most the move of the radius).
+    Elements: rtol * (|x_ref| + S_1), plus the l1 inner band rule of
+    check_bilevel when the innermost level is l1."""
+    x_gpu = np.asarray(x_gpu, np.float64)
+    t = np.asarray(t, np.float64)
+    r = len(levels)
+    assert r >= 2
+    # norm chain V_1 .. V_{r-1} (aggregates over the leading axis)
+    V = [None]
+    cur = np.abs(t)
+    for k in range(r - 1):
+        q = levels[k]
+        cur = cur.sum(0) if q == 0 else (np.sqrt((cur * cur).sum(0)) if q == 1 else cur.max(0))
+        V.append(cur)
+    U = [None] * r
+    for k, c in zip(range(r - 1, 0, -1), chain_ref):
+        U[k] = np.asarray(c, np.float64).reshape(V[k].shape)
+    S = [None] * r
+    S[r - 1] = _near_slack(V[r - 1], U[r - 1], rtol) if levels[r - 1] == 0 else np.zeros_like(V[r - 1])
+    for k in range(r - 2, 0, -1):
+        inh = np.broadcast_to(S[k + 1], V[k].shape)
+        S[k] = inh + (_near_slack(V[k], U[k], rtol) if levels[k] == 0 else 0.0)
+    if chain_gpu is not None:
+        for k, c in zip(range(r - 1, 0, -1), chain_gpu):
+            ug = np.asarray(c, np.float64).reshape(V[k].shape)
+            bad = np.abs(ug - U[k]) > rtol * (np.abs(U[k]) + S[k])
+            assert not bad.any(), f"level {k}: {int(bad.sum())} budgets out of tolerance"
+    tol = rtol * (np.abs(x_ref) + np.broadcast_to(S[1], t.shape))
+    if levels[0] == 0:
+        d0 = t.shape[0]
+        y2, x2 = t.reshape(d0, -1), np.asarray(x_ref, np.float64).reshape(d0, -1)
+        taus = inner_taus(y2, x2)
+        has = np.isfinite(taus) & (taus > 0)
+        tt = np.where(has, taus, 0.0)[None, :]
+        band = has[None, :] & (np.abs(np.abs(y2) - tt) <= rtol * tt)
+        tol = tol + np.where(band, rtol * tt, 0.0).reshape(t.shape)
+    err = np.abs(x_gpu - x_ref)
+    bad = err > tol
+    assert not bad.any(), (f"{int(bad.sum())} elements out of tolerance; worst gpu="
+                           f"{x_gpu.reshape(-1)[np.argmax(err - tol)]!r} ref={x_ref.reshape(-1)[np.argmax(err - tol)]!r}")
+    rel = err / np.maximum(np.abs(x_ref), 1e-300)
+    return {"max_rel": float(rel[x_ref != 0].max()) if np.any(x_ref != 0) else 0.0,
+            "near_entries": int(sum(int((s > 0).sum()) for s in S[1:]))}

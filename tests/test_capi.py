@@ -107,3 +107,16 @@ def test_config5_eta_zeroes_target_fraction():
     from oracle import oracle as O
     u = O.project_ball(v, "1", eta)
     assert int(np.sum(u == 0)) == int(np.floor(0.9 * 512)) + 1
+
+
+def test_device_projectors_reject_unsupported_dtypes():
+    """float16 / bfloat16 / integer tensors must never reach the kernels (they
+    would read and write 8-byte elements through a smaller buffer)."""
+    import torch
+    for dt in (torch.float16, torch.bfloat16, torch.int32, torch.int64, "float16"):
+        with pytest.raises(mp.MpConfigError):
+            mp.BilevelProjector(8, 8, dt)
+        with pytest.raises(mp.MpConfigError):
+            mp.MultilevelProjector((4, 4, 4), "inf,inf,1", dt)
+    with pytest.raises(mp.MpConfigError):
+        mp.BilevelProjector(8, 8, torch.float32, device="cpu")

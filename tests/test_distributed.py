@@ -24,17 +24,16 @@ CASES = [("1", "inf"), ("1", "1"), ("1", "2"), ("2", "inf"), ("inf", "2")]
 class OracleBackend:
     """Local steps on CPU f64 tensors through the C oracle (tests only)."""
 
-    def norms(self, y, q):
-        return torch.from_numpy(O.aggregate(y.numpy(), q).copy())
+    device = torch.device("cpu")
 
-    def outer(self, v, p, eta):
-        return torch.from_numpy(O.project_ball(v.numpy(), p, eta))
+    def norms(self, y, q, out):
+        return out.copy_(torch.from_numpy(O.aggregate(y.numpy(), q).copy()))
+
+    def outer(self, v, p, eta, out):
+        return out.copy_(torch.from_numpy(O.project_ball(v.numpy(), p, eta)))
 
     def apply(self, y, x, q, v, u, flags=0):
-        return torch.from_numpy(O.project_fibers(y.numpy(), q, v.numpy(), u.numpy()))
-
-    def gather(self, v_local, group=None):
-        return distributed.gather_norms(v_local, group)
+        return x.copy_(torch.from_numpy(O.project_fibers(y.numpy(), q, v.numpy(), u.numpy())))
 
 
 def _worker(rank, world, port, outdir):
@@ -51,6 +50,16 @@ def _worker(rank, world, port, outdir):
             np.save(os.path.join(outdir, f"x{i}_r{rank}.npy"), x_local.numpy())
             np.save(os.path.join(outdir, f"u{i}_r{rank}.npy"), u_local.numpy())
             np.save(os.path.join(outdir, f"z{i}_r{rank}.npy"), np.array([z]))
+        # a planned projector reused across radii, equal block widths (no gather compaction)
+        y2 = datagen.uniform(43, (17, 64), -1.0, 1.0, dtype=np.float64)
+        blk = torch.from_numpy(np.ascontiguousarray(y2[:, 32 * rank:32 * (rank + 1)]))
+        proj = distributed.ShardedBilevelProjector(17, 32, torch.float64, "1", "inf", backend=OracleBackend())
+        for k, frac in enumerate((0.05, 0.5)):
+            eta = frac * O.matrix_pq_norm(y2, "1", "inf")
+            out = torch.empty_like(blk)
+            proj(blk, out, eta)
+            np.save(os.path.join(outdir, f"p{k}_r{rank}.npy"), out.numpy())
+            np.save(os.path.join(outdir, f"pz{k}_r{rank}.npy"), np.array([proj.zero_columns()]))
     finally:
         td.destroy_process_group()
 
@@ -69,6 +78,13 @@ def test_sharded_projection_gloo_world2():
         assert np.array_equal(u, ref["budgets"]), (p, q)
         for r in (0, 1):
             assert int(np.load(os.path.join(outdir, f"z{i}_r{r}.npy"))[0]) == ref["zero_columns"]
+    y2 = datagen.uniform(43, (17, 64), -1.0, 1.0, dtype=np.float64)
+    for k, frac in enumerate((0.05, 0.5)):
+        ref = O.bilevel(y2, frac * O.matrix_pq_norm(y2, "1", "inf"), "1", "inf")
+        x = np.concatenate([np.load(os.path.join(outdir, f"p{k}_r{r}.npy")) for r in (0, 1)], axis=1)
+        assert np.array_equal(x.view(np.uint64), ref["X"].view(np.uint64))
+        for r in (0, 1):
+            assert int(np.load(os.path.join(outdir, f"pz{k}_r{r}.npy"))[0]) == ref["zero_columns"]
 
 
 @pytest.mark.gpu
@@ -83,9 +99,10 @@ def test_cuda_backend_simulated_shards_match_single_call():
         outer = {"1": lambda v: v.sum(), "2": lambda v: v.pow(2).sum().sqrt(), "inf": lambda v: v.amax()}[p](colnorm)
         eta = 0.2 * float(outer)
         ys = [y[:, a:b].contiguous() for a, b in blocks]
-        vs = [be.norms(t, mp.norm_code(q)) for t in ys]
+        be.plan(2000, 1800, 3000, mp._capi.MP_F32, mp.norm_code(p), mp.norm_code(q))
+        vs = [be.norms(t, mp.norm_code(q), torch.empty(t.shape[1], dtype=torch.float64, device="cuda")) for t in ys]
         v = torch.cat(vs)
-        u = be.outer(v, mp.norm_code(p), eta)
+        u = be.outer(v, mp.norm_code(p), eta, torch.empty_like(v))
         xs = [be.apply(t, torch.empty_like(t), mp.norm_code(q), vl, u[a:b]) for t, vl, (a, b) in zip(ys, vs, blocks)]
         x = torch.cat(xs, dim=1)
         x1, b1, _ = mp.bilevel_project(y, eta, p, q)
@@ -97,3 +114,32 @@ def test_cuda_backend_simulated_shards_match_single_call():
             torch.testing.assert_close(u, b1, rtol=1e-12, atol=0.0)
         y_h = y.cpu().numpy()
         check_bilevel(x.cpu().numpy(), y_h, O.bilevel(y_h.astype(np.float64), eta, p, q), q)
+
+
+@pytest.mark.gpu
+def test_sharded_projector_nccl_world1_graph_capture():
+    """The planned projector on NCCL (world 1) inside a captured CUDA graph:
+    no host sync and no C-ABI allocation per call, result equal to the
+    single-call projection bit for bit (l_inf maxima are exact)."""
+    import paper_2405_02086_b200 as mp
+    store = td.HashStore()
+    td.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        y = torch.from_numpy(datagen.uniform(44, (3000, 2500), -1.0, 1.0)).cuda()
+        eta = 0.1 * float(y.abs().amax(0).double().sum())
+        proj = distributed.ShardedBilevelProjector(3000, 2500, torch.float32, "1", "inf")
+        x = torch.empty_like(y)
+        proj(y, x, eta)  # warm-up outside capture (NCCL communicator setup)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        x.zero_()
+        with torch.cuda.graph(g):
+            proj(y, x, eta)
+        g.replay()
+        torch.cuda.synchronize()
+        x1, b1, z1 = mp.bilevel_project(y, eta, "1", "inf")
+        assert torch.equal(x.view(torch.int32), x1.view(torch.int32))
+        assert torch.equal(proj.budgets, b1)
+        assert proj.zero_columns() == z1
+    finally:
+        td.destroy_process_group()

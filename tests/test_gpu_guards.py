@@ -46,7 +46,10 @@ class Arena:
 
 
 @pytest.mark.parametrize("dt", ["float32", "float64"])
-@pytest.mark.parametrize("n,m", [(37, 45), (1, 7), (300, 64), (9000, 6), (4097, 24), (13000, 8), (5, 33)])
+# (600, 24) (1000, 8): 64-thread TMA strips; (1500, 16): 128-thread TMA strips;
+# (3000, 8): 256-thread TMA strips (f32); (4097, 24): 512-thread TMA strips (f64)
+@pytest.mark.parametrize("n,m", [(37, 45), (1, 7), (300, 64), (9000, 6), (4097, 24), (13000, 8), (5, 33),
+                                 (600, 24), (1000, 8), (1500, 16), (3000, 8)])
 def test_bilevel_writes_stay_in_bounds(dt, n, m):
     import torch
     lib = _capi.lib()

@@ -13,7 +13,7 @@ import pytest
 import paper_2405_02086_b200 as mp
 from oracle import oracle as O
 from paper_2405_02086_b200 import datagen
-from tests.parity import check_bilevel
+from tests.parity import check_bilevel, check_multilevel
 
 pytestmark = pytest.mark.gpu
 
@@ -66,8 +66,54 @@ def test_golden_multilevel(golden):
         np.testing.assert_allclose(x64, golden[f"ml{i}_x"], rtol=1e-12, atol=1e-15, err_msg=f"case {i}")
         flat = np.concatenate([c.reshape(-1) for c in chain]) if chain else np.zeros(0)
         np.testing.assert_allclose(flat, golden[f"ml{i}_chain"], rtol=1e-12, atol=1e-15, err_msg=f"case {i}")
-        x32 = mp.multilevel_project(t, lv, eta)
-        np.testing.assert_allclose(x32, golden[f"ml{i}_x"], rtol=2e-5, atol=1e-6, err_msg=f"case {i}")
+        x32, chain32 = mp.multilevel_project(t, lv, eta, return_chain=True)
+        assert x32.dtype == np.float32
+        if len(lv) >= 2:  # the per-level §8(c) rule, no absolute slack
+            ref_chain = _split_chain(golden[f"ml{i}_chain"], t.shape)
+            check_multilevel(x32, t, lv, golden[f"ml{i}_x"], ref_chain, chain32)
+        else:
+            np.testing.assert_allclose(x32, golden[f"ml{i}_x"], rtol=1e-5, atol=0.0, err_msg=f"case {i}")
+
+
+def _split_chain(flat, shape):
+    out, off = [], 0
+    for i in range(len(shape) - 1, 0, -1):
+        size = int(np.prod(shape[i:]))
+        out.append(np.asarray(flat[off:off + size]).reshape(shape[i:]))
+        off += size
+    return out
+
+
+MULTI_SPECS_3D = ["1,1,1", "2,inf,1", "inf,1,1", "1,inf,1", "2,2,1", "inf,2,1", "1,1,2"]
+
+
+@pytest.mark.parametrize("spec", MULTI_SPECS_3D)
+@pytest.mark.parametrize("d", [128, 256])
+def test_multilevel_f32_nontrivial_specs(spec, d):
+    """fp32 non-collapsed multi-level specs at size, per-level §8(c) rule
+    against the oracle on the same fp32 values (upcast to f64)."""
+    t = datagen.normal(400 + d, (d, d, d))
+    t64 = t.astype(np.float64)
+    levels = spec.split(",")
+    codes = [mp.norm_code(q) for q in levels]
+    eta = 0.05 * O.multilevel_norm(t64, levels)
+    x, chain = mp.multilevel_project(t, spec, eta, return_chain=True)
+    xr, chain_r = O.multilevel(t64, levels, eta, want_chain=True)
+    rep = check_multilevel(x, t, codes, xr, chain_r, chain)
+    assert rep["max_rel"] < 1e-5
+
+
+@pytest.mark.parametrize("shape", [(16, 24, 32, 48), (32, 32, 32, 32)])
+@pytest.mark.parametrize("spec", ["1,2,inf,1", "inf,1,2,1", "2,1,1,1"])
+def test_multilevel_f32_order4(shape, spec):
+    t = datagen.normal(77, shape)
+    t64 = t.astype(np.float64)
+    levels = spec.split(",")
+    codes = [mp.norm_code(q) for q in levels]
+    eta = 0.05 * O.multilevel_norm(t64, levels)
+    x, chain = mp.multilevel_project(t, spec, eta, return_chain=True)
+    xr, chain_r = O.multilevel(t64, levels, eta, want_chain=True)
+    check_multilevel(x, t, codes, xr, chain_r, chain)
 
 
 def test_golden_vector_balls(golden):
@@ -115,6 +161,24 @@ def test_nonfinite_is_value_error():
     t[1, 2, 3] = np.nan
     with pytest.raises(mp.MpValueError):
         mp.multilevel_project(t, "inf,inf,1", 1.0)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("n,m", [(600, 24), (1500, 16), (3000, 8), (4096, 64)])
+def test_nonfinite_on_l1_strip_routes(dt, n, m):
+    """Non-finite input on the TMA / hybrid l1 strip routes: every CTA leaves
+    early with its strip copies drained; the call reports ValueError, and the
+    next call on the same context is clean."""
+    y = datagen.normal(5, (n, m)).astype(dt)
+    for bad in (np.nan, np.inf):
+        y2 = y.copy()
+        y2[n // 2, m - 1] = bad
+        with pytest.raises(mp.MpValueError):
+            mp.bilevel_project(y2, 1.0, "1", "1")
+    eta = 0.05 * float(np.abs(y.astype(np.float64)).sum())
+    x, _, _ = mp.bilevel_project(y, eta, "1", "1")
+    ref = O.bilevel(y.astype(np.float64), eta, "1", "1")
+    check_bilevel(x, y, ref, "1")
 
 
 # ------------------------------------------------ configs (scaled, oracle)
