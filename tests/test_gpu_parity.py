@@ -6,6 +6,7 @@ oracle finishes in seconds and otherwise through size-independent properties
 (feasibility, idempotence, determinism, in-place == out-of-place).
 """
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -240,6 +241,45 @@ def test_config4_full_trilevel():
     ref = O.bilevel(t64.reshape(256 * 256, 256), eta)
     assert np.array_equal(ref["X"].reshape(t.shape), xr)
     check_bilevel(x.reshape(256 * 256, 256), t.reshape(256 * 256, 256), ref, "inf")
+
+
+def _ref_bilevel_dict(y64, eta, p, q):
+    """The compiled, unmodified reference (oracle/_ref) in the dict shape
+    check_bilevel reads: X, budgets, zero_columns, plus the column norms and
+    the outer l1 threshold recovered from its budgets."""
+    r = O.ref_bilevel(y64, eta, p, q, workers=os.cpu_count() or 1)
+    a = np.abs(y64)
+    v = a.sum(0) if q == "1" else (np.sqrt((a * a).sum(0)) if q == "2" else a.max(0))
+    tau = -1.0
+    if p == "1" and np.any(r["budgets"] > 0) and v.sum() > eta:
+        tau = float(np.max(np.where(r["budgets"] > 0, v - r["budgets"], -np.inf)))
+    return {"X": r["X"], "budgets": r["budgets"], "zero_columns": r["zero_columns"], "v": v, "tau": tau}
+
+
+@pytest.mark.parametrize("case", ["c2_r0.1", "c3_l11", "c3_l12", "c4"])
+def test_config_scale_against_compiled_reference(case):
+    """Full-size parity directly against the compiled reference library (not
+    the C restatement): config 2 at one radius, config 3 l1,1 / l1,2, config 4."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    if case == "c4":
+        t = datagen.config_input(4)
+        t64 = t.astype(np.float64)
+        eta = 0.05 * O.ref_multilevel_norm(t64, ["inf", "inf", "1"])
+        xr, chain_r = O.ref_multilevel(t64, ["inf", "inf", "1"], eta, want_chain=True)
+        x, chain = mp.multilevel_project(t, "inf,inf,1", eta, return_chain=True)
+        check_multilevel(x, t, [2, 2, 0], xr, chain_r, chain)
+        return
+    cfg, p, q, rel = {"c2_r0.1": (2, "1", "inf", 0.1), "c3_l11": (3, "1", "1", 0.05),
+                      "c3_l12": (3, "1", "2", 0.05)}[case]
+    y = datagen.config_input(cfg)
+    y64 = y.astype(np.float64)
+    eta = rel * O.ref_multilevel_norm(y64, [q, p])
+    ref = _ref_bilevel_dict(y64, eta, p, q)
+    del y64
+    x, b, z = run(y, eta, p, q)
+    check_bilevel(x, y, ref, q, zero_cols_gpu=z)
+    assert z == ref["zero_columns"]
 
 
 def test_config5_iteration0_full():
