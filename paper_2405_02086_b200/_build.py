@@ -28,6 +28,10 @@ NVCC_FLAGS = [
     "-shared",
 ]
 CU_SOURCES = ["mp_device.cu", "mp_host.cu"]
+# MP_TUNING_SWITCHES=1 at build time compiles in the A/B route switches
+# (MP_L1_PIPE, MP_L1_TMA, ... read from the environment; tuning builds only).
+if os.environ.get("MP_TUNING_SWITCHES") == "1":
+    NVCC_FLAGS = NVCC_FLAGS + ["-DMP_TUNING_SWITCHES"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:
