@@ -913,7 +913,7 @@ __device__ __forceinline__ double load_norm(const ApplyCols& a, int64_t c) {
 }
 
 // l_inf clamp (proj/src/fiber_kernels.cpp:43-49) / l2 scale (:50-55).
-// `dead` column groups (u == 0) are written as +0 without a read unless
+// `dead` packs (all budgets 0) are written as +0 without a read unless
 // MP_FLAG_EXACT_ZERO_SIGN.
 // f32 l2 runs at 4 CTAs per SM (<= 64 registers): 143.4 vs 145.4 us on config 3
 // l1,2 at the 5 CTAs its 48 registers would allow (a grid of fewer row slots).
@@ -965,19 +965,18 @@ __global__ void __launch_bounds__(kThreads, (Q == kL2 && sizeof(T) == 4) ? 4 : 0
       dead = dead && (A.budgets[c0 + j] == 0.0);
     }
   }
-  // Zero-budget packs are stored without a read, but only when the whole
-  // 16-lane group (256 contiguous bytes) is zero-budget: lines written partly
-  // early by read-free packs and partly late by loading ones are evicted
-  // partially valid and cost DRAM read-modify-writes.  Measured group sizes
-  // (f64 l_inf 4096x16384 K3 / config-5 iteration 0 projection, 90% zero
-  // columns): 1 lane 405 us / 1.13 ms, 2: 183 / 0.65, 8: 175 / 0.54,
-  // 16: 174 / 0.53, 32: 176 / 0.53.  Lanes past m count as dead.
-  {
-    const int lane = threadIdx.x & 31;
-    const unsigned grp = 0xffffu << (lane & 16);
-    const unsigned db = __ballot_sync(__activemask(), dead) | ~__activemask();
-    dead = (db & grp) == grp;
-  }
+  // Zero-budget packs are stored without a read.  Every lane stays in the
+  // one loop below and only its LOAD is predicated on the pack being live,
+  // so each warp store still writes its whole contiguous row segment at
+  // once: lines written partly early (by read-free lanes) and partly late
+  // are evicted partially valid and cost DRAM read-modify-writes (a separate
+  // store-only loop for dead lanes: config-5 iteration 0 1.13 ms per lane,
+  // 0.53 ms per 16-lane group, 0.527 ms like this).  The skipped reads only
+  // pay when a whole 128-byte line is dead: with 10% of the columns alive
+  // at random the L1 asks for 62% of the sectors, but L2 and DRAM serve 96%
+  // (the line-granular fraction, 1 - 0.9^32), whatever the cache operator
+  // (.cs, .cg, .nc.L1::no_allocate measured alike; profiles/r2_zero_skip.txt).
+  // Lanes past m never reach here.
   if (rw.cnt <= 0) return;
   // This CTA's rows are swept LAST-FIRST: K1 swept them first-last in the
   // same resident wave, so the rows it touched last are still in L2 when
@@ -985,14 +984,7 @@ __global__ void __launch_bounds__(kThreads, (Q == kL2 && sizeof(T) == 4) ? 4 : 0
   const int64_t ds = rw.step * m;
   const int64_t last = (rw.r0 + (rw.cnt - 1) * rw.step) * m + c0;
   T* q = x + last;
-  if (dead) {
-    T z[VEC];
-#pragma unroll
-    for (int j = 0; j < VEC; ++j) z[j] = T(0);
-    for (int64_t k = 0; k < rw.cnt; ++k, q -= ds) store_stream<T, VEC>(q, z);
-    tl_end(3);
-    return;
-  }
+  const bool live = !dead;
   // f32 l2 scale: the f64 factor as a float pair (hi + lo), the product
   // y * factor formed in f32 with an exact FMA error term -- full-rate FP32
   // instead of two f32<->f64 converts (1/8 rate) and a DMUL per element.
@@ -1029,7 +1021,9 @@ __global__ void __launch_bounds__(kThreads, (Q == kL2 && sizeof(T) == 4) ? 4 : 0
     T e[U][VEC];
 #pragma unroll
     for (int u = 0; u < U; ++u) {  // one live address per stream
-      load_last<T, VEC>(p, e[u]);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) e[u][j] = T(0);
+      if (live) load_last<T, VEC>(p, e[u]);
       p = step_ptr(p, -ds);
     }
 #pragma unroll
@@ -1042,7 +1036,9 @@ __global__ void __launch_bounds__(kThreads, (Q == kL2 && sizeof(T) == 4) ? 4 : 0
   }
   for (; k < rw.cnt; ++k, p -= ds, q -= ds) {
     T e[VEC];
-    load_last<T, VEC>(p, e);
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) e[j] = T(0);
+    if (live) load_last<T, VEC>(p, e);
 #pragma unroll
     for (int j = 0; j < VEC; ++j) e[j] = op(e[j], j);
     store_stream<T, VEC>(q, e);
