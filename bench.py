@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-f64", action="store_true", help="skip the f64 (drop-in dtype) device leg")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the C++ drop-in e2e leg")
     return ap.parse_args()
 
 
@@ -179,8 +181,67 @@ def run_reference(args, rank):
                          "sample": f"{args.steps} reference bilevel_project calls (ThreadPool workers={used}), "
                                    "1 per step cycling the 4 radii; time includes the API's own output copy"},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_stats": step_stats([1e3 * t for t in per]),
     }
     print(json.dumps(line), flush=True)
+
+
+class SweepTimer:
+    """ONE CUDA graph per step: [L2 flush, projection] x len(etas).  The
+    library records a timing event before each projection's first node and
+    after its last (external event nodes), so the step's projections are
+    timed on the device without the flushes and without per-replay launch
+    overhead.  (No events between the kernels: an event node there would
+    break the PDL edges K1 -> K2 -> K3.)"""
+
+    def __init__(self, torch, lib, proj, y, x, etas, stream, flush):
+        self.torch, self.lib, self.stream = torch, lib, stream
+        self.ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in etas]
+
+        def one_step():
+            for k, e in enumerate(etas):
+                flush.zero_()
+                handles = (C.c_void_p * 4)(C.c_void_p(self.ev[k][0].cuda_event), None, None,
+                                           C.c_void_p(self.ev[k][1].cuda_event))
+                lib.mp_profile_events(handles, 4)
+                proj(y, x, e, stream=stream)
+                lib.mp_profile_events(None, 0)
+
+        with torch.cuda.stream(stream):
+            for row in self.ev:
+                for v in row:
+                    v.record(stream)  # materialise the events before capture
+            one_step()  # eager warm call
+            torch.cuda.synchronize()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=stream):
+                one_step()
+        torch.cuda.synchronize()
+
+    def warm(self, reps):
+        for _ in range(reps):
+            self.graph.replay()
+        self.torch.cuda.synchronize()
+
+    def run(self, steps):
+        """Device ms of each step's projections (the flushes excluded)."""
+        out = []
+        with self.torch.cuda.stream(self.stream):
+            for _ in range(steps):
+                self.graph.replay()
+                self.stream.synchronize()  # the step's events are re-recorded by every replay
+                out.append(sum(a.elapsed_time(b) for a, b in self.ev))
+        return out
+
+    def close(self):
+        del self.graph
+        self.torch.cuda.synchronize()
+
+
+def step_stats(ms):
+    a = np.asarray(ms, np.float64)
+    return {"mean_ms": float(a.mean()), "median_ms": float(np.median(a)), "min_ms": float(a.min()),
+            "p90_ms": float(np.percentile(a, 90)), "max_ms": float(a.max()), "n": int(a.size)}
 
 
 def run_ours(args, rank, world, local_rank):
@@ -215,32 +276,6 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.Stream(dev)
     nproj = len(etas)
     lib = _capi.lib()
-    # ONE CUDA graph per step: [L2 flush, projection] x 4.  The library
-    # records a timing event before each projection's first node and after its
-    # last (external event nodes), so the step's projections are timed on the
-    # device without the flushes and without per-replay launch overhead.  (No
-    # events between the kernels: an event node there would break the PDL
-    # edges K1 -> K2 -> K3.)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nproj)]
-
-    def one_step():
-        for k, e in enumerate(etas):
-            flush.zero_()
-            handles = (C.c_void_p * 4)(C.c_void_p(ev[k][0].cuda_event), None, None, C.c_void_p(ev[k][1].cuda_event))
-            lib.mp_profile_events(handles, 4)
-            proj(y, x, e, stream=stream)
-            lib.mp_profile_events(None, 0)
-
-    with torch.cuda.stream(stream):
-        for row in ev:
-            for v in row:
-                v.record(stream)  # materialise the events before capture
-        one_step()  # eager warm call
-        torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream):
-            one_step()
-    torch.cuda.synchronize()
     # survivors per radius (device info after a plain run)
     f_surv, outer_iters = [], []
     for e in etas:
@@ -252,32 +287,28 @@ def run_ours(args, rank, world, local_rank):
     bytes_step = sum(algo_bytes(n, m, f) for f in f_surv)
     apply_bytes = [4.0 * n * m * (1.0 + f) for f in f_surv]  # K3: surviving reads + full write
 
-    for _ in range(max(3, args.warmup)):
-        graph.replay()
-    torch.cuda.synchronize()
+    sweep = SweepTimer(torch, lib, proj, y, x, etas, stream, flush)
+    sweep.warm(max(3, args.warmup))
     if dist:
         td.barrier()
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.15)
     torch.cuda.synchronize()
-    t_proj = 0.0
     wall0 = torch.cuda.Event(enable_timing=True)
     wall1 = torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         wall0.record(stream)
-        for _ in range(args.steps):
-            graph.replay()
-            stream.synchronize()  # the step's events are re-recorded by every replay
-            for k in range(nproj):
-                t_proj += ev[k][0].elapsed_time(ev[k][1])
+    per_step = sweep.run(args.steps)
+    with torch.cuda.stream(stream):
         wall1.record(stream)
     torch.cuda.synchronize()
     if dist:
         td.barrier()
     clock_info = clocks.stop()
     wall_ms = wall0.elapsed_time(wall1)
-    ms_per_step = t_proj / args.steps
+    sweep.close()
+    ms_per_step = float(np.mean(per_step))
     if dist:
         tt = torch.tensor([ms_per_step], dtype=torch.float64, device=dev)
         td.all_reduce(tt, op=td.ReduceOp.MAX)
@@ -328,7 +359,6 @@ def run_ours(args, rank, world, local_rank):
             if rep > 0:  # the first round warms the eager path
                 k3_ev += [ev3[k][0].elapsed_time(ev3[k][1]) for k in range(nproj)]
     peak, peak_src = peaks()
-    del graph
     k3_ms = float(np.mean(k3_ev))
     k3_bytes = sum(apply_bytes) / nproj
     k3_gbs = k3_bytes / (k3_ms * 1e-3) / 1e9
@@ -348,6 +378,52 @@ def run_ours(args, rank, world, local_rank):
             roofline["traffic"] = json.load(open(traffic_path)).get("bytes_per_launch")
         except Exception:
             pass
+
+    # ---- f64 leg: the same sweep in the C++ drop-in's dtype (DenseTensor is
+    # f64), device-resident, timed like the headline
+    f64_leg = None
+    if not args.no_f64 and rank == 0:
+        y64 = y.double()
+        x64 = torch.empty_like(y64)
+        proj64 = mp.BilevelProjector(n, m, "float64", "1", "inf", dev)
+        sw = SweepTimer(torch, lib, proj64, y64, x64, etas, stream, flush)
+        sw.warm(3)
+        ms64 = sw.run(max(5, min(args.steps, 20)))
+        sw.close()
+        b64 = 2.0 * bytes_step  # 8-byte elements, same survivors
+        st64 = step_stats(ms64)
+        f64_leg = {"value": b64 / (st64["mean_ms"] * 1e-3) / 1e9, "unit": "GB/s",
+                   "pct_hbm": b64 / (st64["mean_ms"] * 1e-3) / 1e9 / peak, "dtype": "f64", "step_stats": st64,
+                   "note": "config 2 sweep on the f64 copy of the same values (the drop-in's dtype), device-resident, "
+                           "L2 flushed before each projection"}
+        del y64, x64, proj64
+        torch.cuda.empty_cache()
+
+    # ---- e2e through the C++ drop-in (the reference's own call shape):
+    # multiproj::bilevel_project(const DenseTensor&, ...) on a pageable host f64
+    # DenseTensor, result returned by value (tests/cpp/dropin_bench.cpp)
+    dropin = None
+    if not args.no_dropin and rank == 0 and world == 1:
+        from paper_2405_02086_b200 import _build
+        try:
+            out = subprocess.run([_build.DROPIN_BENCH, str(n), str(m), "3"] + [str(r) for r in RADII],
+                                 capture_output=True, text=True, timeout=600, check=True).stdout
+            d = json.loads(out)
+            tot_b, tot_t = 0.0, 0.0
+            for r in d["radii"]:
+                secs = sorted(r["seconds"])
+                med = secs[len(secs) // 2]
+                tot_b += algo_bytes(n, m, r["survivors"] / m, s=8)
+                tot_t += med
+            dropin = {"value": tot_b / tot_t / 1e9, "unit": "GB/s", "dtype": "f64",
+                      "h2d_bytes_per_step": len(RADII) * n * m * 8,
+                      "d2h_bytes_per_step": len(RADII) * (n * m * 8 + m * 8),
+                      "ms_per_step": 1e3 * tot_t, "path": "multiproj::bilevel_project(const DenseTensor&, L1, Inf, "
+                      "eta) from libmultiproj_b200.so, pageable f64 host tensor in, DenseTensor out (the reference's "
+                      "call shape; median of 3 calls per radius)",
+                      "vs": "the reference arm times the same call on its CPU library"}
+        except Exception as exc:
+            dropin = {"value": None, "error": str(exc)[:200]}
 
     # ---- e2e through the host-buffer C-ABI (pinned host buffers): the step's
     # radius sweep via mp_bilevel_sweep_host (one upload of Y, four downloads
@@ -456,6 +532,9 @@ def run_ours(args, rank, world, local_rank):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "step_stats": step_stats(per_step),
+            "f64_leg": f64_leg,
+            "e2e_dropin": dropin,
             "clocks": clock_info,
             "gpu_launches": 3 * nproj * args.steps,
         }

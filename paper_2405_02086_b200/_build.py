@@ -49,6 +49,18 @@ def build_cpp_test(out: str) -> str:
     return out
 
 
+DROPIN_BENCH = os.path.join(PKG, "dropin_bench")
+
+
+def build_dropin_bench(out: str = DROPIN_BENCH) -> str:
+    """Compile tests/cpp/dropin_bench.cpp (bench.py's C++ drop-in e2e leg)."""
+    src = os.path.join(ROOT, "tests", "cpp", "dropin_bench.cpp")
+    if _stale(out, [src, DROPIN]):
+        subprocess.run(["g++", "-std=c++20", "-O2", f"-I{INCLUDE}", src, f"-L{PKG}", "-lmultiproj_b200", "-lmp_b200",
+                        "-Wl,-rpath,$ORIGIN", "-o", out], check=True)
+    return out
+
+
 def build_io_test(out: str) -> str:
     """Compile tests/cpp/io_compat.cpp (host-side formats, no GPU calls)."""
     src = os.path.join(ROOT, "tests", "cpp", "io_compat.cpp")
@@ -71,6 +83,7 @@ def build(force: bool = False, verbose: bool = False) -> None:
     if force or _stale(DROPIN, di_deps):
         subprocess.run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", f"-I{INCLUDE}", *di, f"-L{PKG}", "-lmp_b200",
                         "-Wl,-rpath,$ORIGIN", "-o", DROPIN], check=True)
+    build_dropin_bench()
     dg = os.path.join(CSRC, "datagen.c")
     if force or _stale(DATAGEN, [dg]):
         subprocess.run(["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fPIC", "-shared", dg,

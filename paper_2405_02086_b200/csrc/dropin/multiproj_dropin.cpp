@@ -11,6 +11,8 @@
 #include <sstream>
 #include <thread>
 
+#include <sys/mman.h>
+
 #include "mp_cuda.h"
 #include "multiproj/bilevel.hpp"
 #include "multiproj/dispatch.hpp"
@@ -80,6 +82,34 @@ DenseTensor::DenseTensor(std::vector<std::size_t> shape, std::vector<double> dat
     throw ValueError("non-finite tensor entry");
   fibers_ = data_.size() / shape_.front();
 }
+
+DenseTensor::DenseTensor(Unchecked, std::vector<std::size_t> shape, std::vector<double> data)
+    : shape_(std::move(shape)), data_(std::move(data)) {
+  fibers_ = data_.size() / shape_.front();
+}
+
+// Result tensors: a fresh host buffer (transparent huge pages requested
+// before the first touch -- 4 KB first-touch faults cost 300 ms on an 800 MB
+// result) and the unchecked constructor (the projections of finite input
+// are finite; the reference copies Y without a re-check).
+struct TensorFactory {
+  static std::vector<double> buffer(std::size_t n) {
+    std::vector<double> v;
+    v.reserve(n);
+    const std::size_t bytes = n * sizeof(double);
+    if (bytes >= (std::size_t(8) << 20)) {
+      const uintptr_t a = (reinterpret_cast<uintptr_t>(v.data()) + (std::size_t(2) << 20) - 1) &
+                          ~((std::size_t(2) << 20) - 1);
+      const uintptr_t e = reinterpret_cast<uintptr_t>(v.data()) + bytes;
+      if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);
+    }
+    v.resize(n);
+    return v;
+  }
+  static DenseTensor result(std::vector<std::size_t> shape, std::vector<double> data) {
+    return DenseTensor(DenseTensor::Unchecked{}, std::move(shape), std::move(data));
+  }
+};
 
 DenseTensor DenseTensor::zeros(std::vector<std::size_t> shape) {
   std::size_t total = 1;
@@ -164,14 +194,15 @@ BilevelResult bilevel_project(const DenseTensor& y, Norm p, Norm q, double eta, 
   if (y.order() != 2) throw ShapeError("bilevel_project requires order 2");
   check_radius(eta);
   const std::size_t n = y.fiber_length(), m = y.fiber_count();
-  std::vector<double> x(y.size()), budgets(m);
+  std::vector<double> x = TensorFactory::buffer(y.size()), budgets(m);
   int64_t zeros = 0;
   double tau = 0.0;
   // Exact zero signs: the drop-in reproduces the reference's bytes.
   check(mp_bilevel_project_host(nullptr, y.data().data(), x.data(), MP_F64, static_cast<int64_t>(n),
                                 static_cast<int64_t>(m), to_mp(p), to_mp(q), eta, budgets.data(), &zeros, &tau,
                                 MP_FLAG_EXACT_ZERO_SIGN));
-  return BilevelResult{DenseTensor(y.shape(), std::move(x)), std::move(budgets), static_cast<std::size_t>(zeros)};
+  return BilevelResult{TensorFactory::result(y.shape(), std::move(x)), std::move(budgets),
+                       static_cast<std::size_t>(zeros)};
 }
 
 BilevelResult bilevel_project_l1inf(const DenseTensor& y, double eta, ThreadPool* pool) {
@@ -217,17 +248,17 @@ MultilevelResult run_multilevel(const DenseTensor& t, const NormSpec& nu, double
     mi *= t.shape()[i];
     chain_len += mi;
   }
-  std::vector<double> x(t.size()), chain(std::max<std::size_t>(chain_len, 1));
+  std::vector<double> x = TensorFactory::buffer(t.size()), chain(std::max<std::size_t>(chain_len, 1));
   check(mp_multilevel_project_host(nullptr, t.data().data(), x.data(), MP_F64, shape.data(), order, levels.data(),
                                    order, eta, want_chain ? chain.data() : nullptr, MP_FLAG_EXACT_ZERO_SIGN));
-  MultilevelResult r{DenseTensor(t.shape(), x), {}};
+  MultilevelResult r{TensorFactory::result(t.shape(), std::move(x)), {}};
   if (!want_chain) return r;
   std::size_t off = 0;
   for (int i = order - 1; i >= 1; --i) {
     std::vector<std::size_t> sh(t.shape().begin() + i, t.shape().end());
     std::size_t sz = 1;
     for (std::size_t d : sh) sz *= d;
-    r.budget_chain.emplace_back(sh, std::vector<double>(chain.begin() + off, chain.begin() + off + sz));
+    r.budget_chain.push_back(TensorFactory::result(sh, std::vector<double>(chain.begin() + off, chain.begin() + off + sz)));
     off += sz;
   }
   r.budget_chain.push_back(r.X);
@@ -290,11 +321,11 @@ EuclidResult euclid_project_l1inf(const DenseTensor& y, double eta) {
   if (y.order() != 2) throw ShapeError("euclid_project_l1inf requires order 2");
   check_radius(eta);
   const std::size_t n = y.fiber_length(), m = y.fiber_count();
-  std::vector<double> x(y.size()), budgets(m);
+  std::vector<double> x = TensorFactory::buffer(y.size()), budgets(m);
   double theta = 0.0;
   check(mp_euclid_project_host(nullptr, y.data().data(), x.data(), MP_F64, static_cast<int64_t>(n),
                                static_cast<int64_t>(m), eta, budgets.data(), &theta));
-  return EuclidResult{DenseTensor(y.shape(), std::move(x)), ColumnBudgetSolution{std::move(budgets), theta}};
+  return EuclidResult{TensorFactory::result(y.shape(), std::move(x)), ColumnBudgetSolution{std::move(budgets), theta}};
 }
 
 double clip_cost(const DenseTensor& y, std::span<const double> budgets) {
