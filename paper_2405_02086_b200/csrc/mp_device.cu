@@ -722,8 +722,11 @@ mp_status check_multi_args(const void* t, const void* x, mp_dtype dt, const int6
 // (proj/src/euclidean.cpp:82-170; kernels in mp_euclid.cuh)
 struct EuclidWs {
   mp_info* info;
-  void* mags;         // |Y| column-major, sorted per column
-  mpk::DD* pref;      // prefix sums, column-major
+  void* mags;         // |Y| column-major (stride ld), sorted per column
+  mpk::DD* offs;      // double-double prefix offsets every 32 ranks (stride ldo)
+  double* fb;         // each chunk's first breakpoint (stride ldo)
+  void* tmp;          // merge buffer for a batch of long columns (n > one CTA's sort)
+  int64_t ld, ldo, batch;
   double* colmax;
   double* budgets;
   void* colp;
@@ -732,13 +735,24 @@ struct EuclidWs {
 
 int pow2_at_least(int64_t n);
 
-// The sorted columns are P2-strided (mpk::EuLayout).
+template <typename T>
+int64_t eu_merge_batch(int64_t n, int64_t m, int64_t ld) {
+  if (n <= mpk::eu_sort_cap<T>()) return 0;
+  // long columns merge through a buffer of at most ~1/4 of the tensor
+  return std::max<int64_t>(1, std::min<int64_t>(m, (m + 3) / 4));
+}
+
 EuclidWs carve_euclid(Carve& c, mp_dtype dt, int64_t n, int64_t m) {
   EuclidWs w{};
-  const size_t ld = static_cast<size_t>(std::max(64, pow2_at_least(n)));
+  const size_t s = dtype_size(dt);
+  w.ld = (n + 3) & ~int64_t(3);  // 16-byte aligned columns
+  w.ldo = (n + mpk::kEuChunk - 1) / mpk::kEuChunk;
+  w.batch = dt == MP_F32 ? eu_merge_batch<float>(n, m, w.ld) : eu_merge_batch<double>(n, m, w.ld);
   w.info = c.take<mp_info>(1);
-  w.mags = c.take<char>(ld * m * dtype_size(dt));
-  w.pref = c.take<mpk::DD>(ld * m);
+  w.mags = c.take<char>(static_cast<size_t>(w.ld) * m * s);
+  w.offs = c.take<mpk::DD>(static_cast<size_t>(w.ldo) * m);
+  w.fb = c.take<double>(static_cast<size_t>(w.ldo) * m);
+  w.tmp = w.batch ? c.take<char>(static_cast<size_t>(w.ld) * w.batch * s) : nullptr;
   w.colmax = c.take<double>(m);
   w.budgets = c.take<double>(m);
   w.colp = c.take<double>(m);
@@ -752,37 +766,16 @@ int pow2_at_least(int64_t n) {
   return p;
 }
 
-template <typename T>
-bool euclid_fits(int64_t n) {
-  const size_t P2 = static_cast<size_t>(std::max(64, pow2_at_least(n)));
-  return P2 <= 32u * mpk::kEuSortThreads && P2 * sizeof(T) <= mpk::kEuSortSmemMax;
-}
-
-template <typename T, int E>
-cudaError_t launch_eu_sort(T* mags, mpk::DD* pref, int64_t n, int64_t m, int P2, int nt, size_t smem,
-                           const mp_info* inf, cudaStream_t s) {
-  static std::atomic<uint64_t> done{0};
-  const cudaError_t attr = mpi::once_per_device(done, [] {
-    return cudaFuncSetAttribute(mpk::k_eu_sort<T, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(mpk::kEuSortSmemMax));
-  });
-  if (attr != cudaSuccess) return attr;
-  mpk::k_eu_sort<T, E><<<static_cast<unsigned>(m), nt, smem, s>>>(mags, pref, n, P2, inf);
-  return cudaGetLastError();
-}
-
-// Radix-sorted columns: CUB's temp storage is dynamic shared memory.
 template <typename T, int NT>
-cudaError_t launch_eu_radix(T* mags, mpk::DD* pref, int64_t n, int64_t m, const mp_info* inf, cudaStream_t s) {
-  using Sort = cub::BlockRadixSort<typename mpk::BitsT<T>::type, NT, 16, cub::NullType, mpk::kEuRadixBits>;
-  constexpr size_t smem = sizeof(typename Sort::TempStorage);
+cudaError_t launch_eu_block(T* mags, const EuclidWs& w, int64_t n, int64_t m, const mp_info* inf, cudaStream_t s) {
+  constexpr size_t smem = mpk::EuBlock<T, NT>::kSmem;
   static std::atomic<uint64_t> done{0};
-  const cudaError_t attr = mpi::once_per_device(done, [] {
-    return cudaFuncSetAttribute(mpk::k_eu_sort_radix<T, NT, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const cudaError_t a = mpi::once_per_device(done, [] {
+    return cudaFuncSetAttribute(mpk::k_eu_sort_block<T, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem));
   });
-  if (attr != cudaSuccess) return attr;
-  mpk::k_eu_sort_radix<T, NT, 16><<<static_cast<unsigned>(m), NT, smem, s>>>(mags, pref, n, inf);
+  if (a != cudaSuccess) return a;
+  mpk::k_eu_sort_block<T, NT><<<static_cast<unsigned>(m), NT, smem, s>>>(mags, w.ld, n, w.offs, w.fb, w.ldo, inf);
   return cudaGetLastError();
 }
 
@@ -795,34 +788,50 @@ mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, doubl
   MP_CUDA_TRY(cudaMemsetAsync(inf, 0, sizeof(mp_info), s));
   T* mags = static_cast<T*>(w.mags);
   mpk::k_eu_gather<T><<<dim3(static_cast<unsigned>((m + 31) / 32), static_cast<unsigned>((n + 31) / 32)), dim3(32, 8),
-                        0, s>>>(y, n, m, mags, static_cast<int64_t>(std::max(64, pow2_at_least(n))), inf);
+                        0, s>>>(y, n, m, mags, w.ld, inf);
   MP_CUDA_TRY(cudaGetLastError());
-  // 16 keys per thread (32 beyond 16384): most of the network runs in
-  // registers and shuffles; small columns keep one warp
-  const int P2 = std::max(64, pow2_at_least(n));
-  const int ek = P2 >= 512 ? std::max(16, P2 / mpk::kEuSortThreads) : P2 / 32;
-  const int nt = P2 / ek;
-  const size_t smem = static_cast<size_t>(P2) * sizeof(T);
-  // radix-sorted columns (cub::BlockRadixSort, 16 keys per thread) for
-  // 1024 <= P2 <= 16384; MP_EU_SORT=bitonic keeps the network (A/B aid)
-  static const bool bitonic_only = [] {
-    const char* e = mpk::mp_tuning_env("MP_EU_SORT");
-    return e && std::strcmp(e, "bitonic") == 0;
-  }();
-  if (!bitonic_only && ek == 16 && nt >= 64 && nt <= 1024) {
+  static std::atomic<uint64_t> done{0};
+  MP_CUDA_TRY(mpi::once_per_device(done, [] {
+    return cudaFuncSetAttribute(mpk::k_eu_sort<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(mpk::kEuSortSmemMax));
+  }));
+  // columns that fit one CTA: sorted whole (+ prefix offsets); longer
+  // columns: power-of-two runs, merged pairwise through w.tmp
+  if (n <= (sizeof(T) == 4 ? 16 * 1024 : 8 * 1024)) {  // f64 at 1024 x 16 keys exceeds shared memory
+    int nt = 64;
+    while (nt * 16 < n) nt *= 2;
     switch (nt) {
-      case 64: MP_CUDA_TRY((launch_eu_radix<T, 64>(mags, w.pref, n, m, inf, s))); break;
-      case 128: MP_CUDA_TRY((launch_eu_radix<T, 128>(mags, w.pref, n, m, inf, s))); break;
-      case 256: MP_CUDA_TRY((launch_eu_radix<T, 256>(mags, w.pref, n, m, inf, s))); break;
-      case 512: MP_CUDA_TRY((launch_eu_radix<T, 512>(mags, w.pref, n, m, inf, s))); break;
-      default: MP_CUDA_TRY((launch_eu_radix<T, 1024>(mags, w.pref, n, m, inf, s))); break;
+      case 64: MP_CUDA_TRY((launch_eu_block<T, 64>(mags, w, n, m, inf, s))); break;
+      case 128: MP_CUDA_TRY((launch_eu_block<T, 128>(mags, w, n, m, inf, s))); break;
+      case 256: MP_CUDA_TRY((launch_eu_block<T, 256>(mags, w, n, m, inf, s))); break;
+      case 512: MP_CUDA_TRY((launch_eu_block<T, 512>(mags, w, n, m, inf, s))); break;
+      default: MP_CUDA_TRY((launch_eu_block<T, 1024>(mags, w, n, m, inf, s))); break;
     }
-  } else switch (P2 / nt) {
-    case 2: MP_CUDA_TRY((launch_eu_sort<T, 2>(mags, w.pref, n, m, P2, nt, smem, inf, s))); break;
-    case 4: MP_CUDA_TRY((launch_eu_sort<T, 4>(mags, w.pref, n, m, P2, nt, smem, inf, s))); break;
-    case 8: MP_CUDA_TRY((launch_eu_sort<T, 8>(mags, w.pref, n, m, P2, nt, smem, inf, s))); break;
-    case 16: MP_CUDA_TRY((launch_eu_sort<T, 16>(mags, w.pref, n, m, P2, nt, smem, inf, s))); break;
-    default: MP_CUDA_TRY((launch_eu_sort<T, 32>(mags, w.pref, n, m, P2, nt, smem, inf, s))); break;
+  } else {
+  const bool whole = n <= mpk::eu_sort_cap<T>();
+  const int64_t run = whole ? n : mpk::eu_run_len<T>();
+  const int64_t runs = (n + run - 1) / run;
+  const size_t smem = mpk::kEuHistBytes + 2 * static_cast<size_t>((run + 3) & ~int64_t(3)) * sizeof(T);
+  mpk::k_eu_sort<T><<<dim3(static_cast<unsigned>(runs), static_cast<unsigned>(m)), mpk::kEuSortThreads, smem, s>>>(
+      mags, w.ld, n, run, w.offs, w.fb, w.ldo, inf);
+  MP_CUDA_TRY(cudaGetLastError());
+  if (!whole) {
+    T* tmp = static_cast<T*>(w.tmp);
+    const int64_t tile = static_cast<int64_t>(mpk::kEuMergeThreads) * mpk::kEuMergeE;
+    for (int64_t j0 = 0; j0 < m; j0 += w.batch) {
+      const int64_t nb = std::min(w.batch, m - j0);
+      T* cols = mags + j0 * w.ld;
+      for (int64_t width = run; width < n; width *= 2) {
+        mpk::k_eu_merge<T><<<dim3(static_cast<unsigned>((n + tile - 1) / tile), static_cast<unsigned>(nb)),
+                             mpk::kEuMergeThreads, 0, s>>>(cols, tmp, w.ld, n, width, inf);
+        MP_CUDA_TRY(cudaGetLastError());
+        MP_CUDA_TRY(cudaMemcpyAsync(cols, tmp, static_cast<size_t>(nb) * w.ld * sizeof(T), cudaMemcpyDeviceToDevice,
+                                    s));
+      }
+    }
+    mpk::k_eu_prefix<T><<<static_cast<unsigned>(m), 256, 0, s>>>(mags, w.ld, n, w.offs, w.fb, w.ldo, inf);
+    MP_CUDA_TRY(cudaGetLastError());
+  }
   }
   // cooperative search grid: every CTA co-resident
   static int occ = -1;
@@ -832,13 +841,13 @@ mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, doubl
                                              static_cast<int64_t>(sm_count()) * std::max(1, std::min(occ, 2))));
   G = std::max(1, std::min(G, mpk::kEuMaxCtas));
   const T* cm = mags;
-  const mpk::DD* cp = w.pref;
+  const mpk::DD* co = w.offs;
+  const double* cf = w.fb;
   double* colmax = w.colmax;
+  double* coltot = static_cast<double*>(w.colp);  // scratch until launch_colparams
   mpk::EuScratch* sc = w.sc;
-  mpk::EuLayout lay{P2, 0, 0};
-  while ((1 << lay.lge) < ek) ++lay.lge;
-  while ((1 << lay.lgnt) < nt) ++lay.lgnt;
-  void* args[] = {&cm, &cp, &n, &m, &lay, &eta, &colmax, &u, &inf, &sc};
+  int64_t ld = w.ld, ldo = w.ldo;
+  void* args[] = {&cm, &co, &cf, &n, &m, &ld, &ldo, &eta, &colmax, &u, &coltot, &inf, &sc};
   MP_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(mpk::k_eu_search<T>), dim3(G),
                                           dim3(mpk::kEuSearchThreads), args, 0, s));
   if (eta == 0.0) {  // the reference returns DenseTensor::zeros (+0.0 everywhere)
@@ -1024,7 +1033,6 @@ mp_status mp_project_fibers(const void* y, void* x, mp_dtype dtype, int64_t n, i
 
 size_t mp_euclid_workspace_size(mp_dtype dtype, int64_t n, int64_t m) {
   if (n < 1 || m < 1 || !dtype_ok(dtype)) return 0;
-  if (dtype == MP_F32 ? !euclid_fits<float>(n) : !euclid_fits<double>(n)) return 0;
   Carve c(nullptr, 0);
   carve_euclid(c, dtype, n, m);
   return c.off + 256;
@@ -1036,8 +1044,6 @@ mp_status mp_euclid_project(const void* y, void* x, mp_dtype dtype, int64_t n, i
   if (!dtype_ok(dtype)) return fail(MP_ERR_CONFIG, "unknown dtype code");
   if (n < 1 || m < 1) return fail(MP_ERR_SHAPE, "euclid_project_l1inf requires a non-empty order-2 tensor");
   if (!(eta >= 0.0) || !std::isfinite(eta)) return fail(MP_ERR_VALUE, "radius must be a finite nonnegative real");
-  if (dtype == MP_F32 ? !euclid_fits<float>(n) : !euclid_fits<double>(n))
-    return fail(MP_ERR_UNSUPPORTED, "euclid_project_l1inf: column length beyond the shared-memory sort");
   if (!y || !x || !workspace) return fail(MP_ERR_WORKSPACE, "null pointer");
   Carve c(workspace, workspace_bytes);
   EuclidWs w = carve_euclid(c, dtype, n, m);

@@ -11,29 +11,20 @@
 //  EK0 k_eu_gather   |Y| transposed into column-major order (32x32 tiles,
 //                    both sides coalesced) + the finiteness check
 //                    (tensor.cpp:40-41);
-//  EK1 k_eu_sort     one CTA per column: bitonic sort (descending) in
-//                    registers / shuffles / shared memory, then the
-//                    double-double prefix sums P_k (the reference's long
-//                    double, euclidean.cpp:41-46);
-//  EK2 k_eu_search   a cooperative grid: the feasibility test (l1,inf norm
-//                    <= eta, :95-100) and Newton's iteration on the convex,
-//                    decreasing, piecewise-linear S from theta = 0: each step
-//                    solves the current linear segment exactly,
-//                    theta' = (sum_j P_k/k - eta) / (sum_j 1/k) -- the
-//                    reference's segment solve (:125-141) -- and stops when
-//                    theta' lies inside that segment [max t_k, min t_{k+1}],
-//                    i.e. on the segment the reference's breakpoint bisection
-//                    (:103-123) brackets.  Newton from the left of a convex
-//                    decreasing function never overshoots, so the iteration
-//                    is monotone and finite.  Each column's segment index is
-//                    a binary search over its breakpoints (upper_bound,
-//                    :19-26).  Budgets u_j = max(0, (P_k - theta)/k) (:143-149);
-//  EK3               the l_inf clip at u_j: the bi-level K3 apply kernel.
+//  EK1 k_eu_sort     per column (or per run of a long column), an LSD radix
+//                    sort of the |y| bit patterns in shared memory written
+//                    here (8-bit digits; per-warp digit histograms, stable
+//                    ranks from per-bit ballots), then -- for a whole
+//                    column -- double-double prefix offsets every 32 ranks
+//                    (the reference's long double P_k, euclidean.cpp:41-46;
+//                    P_k itself is re-summed from the chunk's offset);
+//  EK1b k_eu_merge   columns longer than one CTA's shared memory: sorted
+//                    runs merged pairwise in global memory (merge path),
+//                    then k_eu_prefix writes their chunk offsets;
 // Sums are deterministic (fixed trees, CTA partials reduced in CTA order).
 #pragma once
 
 #include <cub/block/block_radix_sort.cuh>
-
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -42,14 +33,28 @@
 
 namespace mpk {
 
-constexpr int kEuSortThreads = 1024;
-#ifndef MP_EU_RADIX_BITS
-#define MP_EU_RADIX_BITS 4
-#endif
-constexpr int kEuRadixBits = MP_EU_RADIX_BITS;  // digit width of the column radix sort
 constexpr int kEuSearchThreads = 256;
 constexpr int kEuMaxCtas = 1024;
+constexpr int kEuChunk = 32;           // ranks per double-double prefix offset
+constexpr int kEuSortThreads = 512;    // 16 warps
+constexpr int kEuSortWarps = kEuSortThreads / 32;
+constexpr int kEuDigits = 256;         // 8-bit radix digits
 constexpr size_t kEuSortSmemMax = 200 * 1024;
+constexpr size_t kEuHistBytes = static_cast<size_t>(kEuSortWarps) * kEuDigits * sizeof(int);
+constexpr int kEuMergeThreads = 256, kEuMergeE = 8;  // merge tile: 2048 outputs
+
+// Keys one sort CTA holds (two ping-pong buffers + the histograms), and the
+// power-of-two run length long columns are cut into.
+template <typename T>
+constexpr int64_t eu_sort_cap() {
+  return static_cast<int64_t>((kEuSortSmemMax - kEuHistBytes) / (2 * sizeof(T))) & ~int64_t(31);
+}
+template <typename T>
+constexpr int64_t eu_run_len() {
+  int64_t r = 1;
+  while (2 * r <= eu_sort_cap<T>()) r *= 2;
+  return r;
+}
 
 struct EuPart {
   DD a, b;         // sum_j P_k/k, sum_j 1/k over the active columns
@@ -61,21 +66,6 @@ struct EuPart {
 struct EuScratch {
   EuPart part[2][kEuMaxCtas];
   long long zero[kEuMaxCtas];
-};
-
-// Sorted-column layout.  Column j occupies [j*ld, j*ld + ld), ld = P2 (the
-// sort's power of two).  Rank r (0-based, descending) of a column sorted by
-// NT threads holding E keys each (thread t: ranks t*E .. t*E+E-1) lives at
-// slot (r % E) * NT + r / E: the sort's stores -- and the unsorted loads --
-// are coalesced across a warp (rank-contiguous stores were 32 scattered
-// sectors per warp instruction).
-struct EuLayout {
-  int64_t ld;  // column stride (P2)
-  int lge;     // log2 E
-  int lgnt;    // log2 NT
-  __device__ __forceinline__ int64_t slot(int64_t r) const {
-    return ((r & ((1 << lge) - 1)) << lgnt) + (r >> lge);
-  }
 };
 
 // ------------------------------------------------------------------- EK0
@@ -105,177 +95,302 @@ __global__ void __launch_bounds__(256) k_eu_gather(const T* __restrict__ y, int6
 }
 
 // ------------------------------------------------------------------- EK1
-// Bitonic sort, descending, of P2 = NT * E keys: thread t holds keys
-// t*E .. t*E+E-1 in registers.  Partner distance d < E: inside the thread;
-// d < 32E: the same register of lane ^ (d/E), by shuffle; larger d: one
-// shared-memory round trip in an [E][NT] layout (conflict-free).  Then the
-// double-double prefix sums P_k (the reference's long double,
-// euclidean.cpp:41-46) over the thread-contiguous chunks: a block scan of the
-// chunk totals and one more pass over the registers.
-template <typename T>
-__device__ __forceinline__ T tmax(T a, T b) {
-  if constexpr (sizeof(T) == 4) return fmaxf(a, b);
-  else return fmax(a, b);
-}
-template <typename T>
-__device__ __forceinline__ T tmin(T a, T b) {
-  if constexpr (sizeof(T) == 4) return fminf(a, b);
-  else return fmin(a, b);
-}
-// keys are finite and >= -1 (padding): min / max are branch-free selects
-template <typename T>
-__device__ __forceinline__ void bitonic_keep(T& v, T o, bool take_max) {
-  const T hi = tmax(v, o), lo = tmin(v, o);
-  v = take_max ? hi : lo;
+template <typename K>
+__device__ __forceinline__ double eu_key_value(K k) {
+  if constexpr (sizeof(K) == 4) return static_cast<double>(__uint_as_float(k));
+  else return __longlong_as_double(static_cast<long long>(k));
 }
 
-// Store the sorted column and its double-double prefix sums P_k (the
-// reference's long double, euclidean.cpp:41-46): chunk totals, warp scan,
-// warp totals, block offsets, one more pass over the registers.
-template <typename T, int E>
-__device__ __forceinline__ void eu_store_prefix(const T (&v)[E], T* __restrict__ col, DD* __restrict__ pc, int64_t n,
-                                                DD* wsum) {
-  const int NT = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // rank tid*E + e -> slot e*NT + tid (EuLayout)
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int i = tid * E + e;
-    if (i < n) col[e * NT + tid] = v[e];
+// Double-double prefix offsets of a sorted column: offs[c] = a_0 + ... +
+// a_{32c - 1} (exclusive), chunk sums by warp trees, the chunk scan by warp
+// 0 (contiguous chunk ranges per lane, then a lane scan) -- fixed orders,
+// deterministic.  `val(i)` reads rank i; `cs` holds >= ceil(len / 32) DDs.
+__device__ __forceinline__ DD dd_sub(DD a, DD b) { return dd_add(a, DD{-b.hi, -b.lo}); }
+
+// First breakpoint of every chunk, t_k at k = 32c + 1 (euclidean.cpp:44-45),
+// from the chunk offsets: the search bisects these (a dense, L2-resident
+// array) instead of re-summing prefixes.  Call after eu_scan_offsets.
+template <typename V>
+__device__ __forceinline__ void eu_first_breaks(V val, int64_t len, const DD* offs, double* fb) {
+  __syncthreads();  // offs were written by warp 0
+  const int64_t nch = (len + kEuChunk - 1) / kEuChunk;
+  for (int64_t c = threadIdx.x; c < nch; c += blockDim.x) {
+    const double a = val(c * kEuChunk), k = static_cast<double>(c * kEuChunk + 1);
+    const DD pk = dd_add(offs[c], a);
+    const double p = k * a, pe = fma(k, a, -p);
+    const DD t = dd_sub(pk, DD{p, pe});
+    fb[c] = t.hi + t.lo;
   }
-  // prefix sums: chunk totals, warp scan, warp totals, block offsets
-  DD s{0.0, 0.0};
-#pragma unroll
-  for (int e = 0; e < E; ++e)
-    if (tid * E + e < n) s = dd_add(s, static_cast<double>(v[e]));
-  DD inc = s;  // inclusive warp scan
+}
+
+// Exclusive double-double scan of nch chunk sums cs[] into offs[] by warp 0:
+// contiguous chunk ranges per lane, then a lane scan (fixed orders,
+// deterministic).  cs may alias offs: each entry is read before it is
+// overwritten, and lanes own disjoint ranges.
+__device__ __forceinline__ void eu_scan_offsets(const DD* cs, int64_t nch, DD* offs) {
+  const int lane = threadIdx.x & 31;
+  if ((threadIdx.x >> 5) != 0) return;
+  const int64_t per = (nch + 31) / 32, c0 = lane * per, c1 = min(nch, c0 + per);
+  DD t{0.0, 0.0};
+  for (int64_t c = c0; c < c1; ++c) t = dd_add(t, cs[c]);
+  DD inc = t;  // inclusive lane scan
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const DD w{__shfl_up_sync(0xffffffffu, inc.hi, o), __shfl_up_sync(0xffffffffu, inc.lo, o)};
     if (lane >= o) inc = dd_add(w, inc);
   }
-  if (lane == 31) wsum[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    DD t = lane < (NT >> 5) ? wsum[lane] : DD{0.0, 0.0};
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const DD w{__shfl_up_sync(0xffffffffu, t.hi, o), __shfl_up_sync(0xffffffffu, t.lo, o)};
-      if (lane >= o) t = dd_add(w, t);
-    }
-    wsum[lane] = t;  // inclusive over warps
-  }
-  __syncthreads();
-  DD run = warp > 0 ? wsum[warp - 1] : DD{0.0, 0.0};
-  const DD ex{__shfl_up_sync(0xffffffffu, inc.hi, 1), __shfl_up_sync(0xffffffffu, inc.lo, 1)};
-  if (lane > 0) run = dd_add(run, ex);
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int i = tid * E + e;
-    if (i < n) {
-      run = dd_add(run, static_cast<double>(v[e]));
-      pc[e * NT + tid] = run;
-    }
+  DD run{__shfl_up_sync(0xffffffffu, inc.hi, 1), __shfl_up_sync(0xffffffffu, inc.lo, 1)};
+  if (lane == 0) run = DD{0.0, 0.0};
+  for (int64_t c = c0; c < c1; ++c) {
+    const DD x = cs[c];
+    offs[c] = run;
+    run = dd_add(run, x);
   }
 }
 
-template <typename T, int E>
-__global__ void __launch_bounds__(kEuSortThreads) k_eu_sort(T* __restrict__ mags, DD* __restrict__ pref, int64_t n,
-                                                            int P2, const mp_info* __restrict__ info) {
-  // column stride P2 (EuLayout); the unsorted keys are read striped
-  // (coalesced): the network does not care which thread starts with which key
-  if (info->status != MP_OK) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sk = reinterpret_cast<T*>(smem_raw);  // [E][NT]
-  __shared__ DD wsum[32];
-  const int NT = blockDim.x, tid = threadIdx.x, lane = tid & 31;
-  const int64_t j = blockIdx.x;
-  T* col = mags + j * P2;
-  T v[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int i = e * NT + tid;
-    v[e] = i < n ? col[i] : T(-1);  // padding sorts last
+// Double-double prefix offsets of a sorted column: offs[c] = a_0 + ... +
+// a_{32c - 1} (exclusive): chunk sums by warp trees, then eu_scan_offsets.
+// `val(i)` reads rank i; `cs` holds >= ceil(len / 32) DDs (may be offs).
+template <typename V>
+__device__ __forceinline__ void eu_prefix_offsets(V val, int64_t len, DD* cs, DD* offs) {
+  const int NT = blockDim.x, NW = NT / 32, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t nch = (len + kEuChunk - 1) / kEuChunk;
+  for (int64_t c = warp; c < nch; c += NW) {
+    const int64_t i = c * kEuChunk + lane;
+    DD v{i < len ? val(i) : 0.0, 0.0};
+    v = warp_reduce_dd(v);
+    if (lane == 0) cs[c] = v;
   }
-  for (int k = 2; k <= P2; k <<= 1) {
-    int d = k >> 1;
-    for (; d >= 32 * E; d >>= 1) {  // shared memory
-#pragma unroll
-      for (int e = 0; e < E; ++e) sk[e * NT + tid] = v[e];
-      __syncthreads();
-      const int pt = tid ^ (d / E);
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int i = tid * E + e;
-        const bool lower = tid < pt, desc = (i & k) == 0;
-        bitonic_keep(v[e], sk[e * NT + pt], lower == desc);
-      }
-      __syncthreads();
-    }
-    for (; d >= E; d >>= 1) {  // shuffles
-      const int dl = d / E;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int i = tid * E + e;
-        const T o = __shfl_xor_sync(0xffffffffu, v[e], dl);
-        const bool lower = (lane & dl) == 0, desc = (i & k) == 0;
-        bitonic_keep(v[e], o, lower == desc);
-      }
-    }
-#pragma unroll
-    for (int dd = E / 2; dd >= 1; dd >>= 1) {  // registers
-      if (dd >= k) continue;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        if (e & dd) continue;
-        const int i = tid * E + e;
-        const bool desc = (i & k) == 0;
-        const T hi = tmax(v[e], v[e + dd]), lo = tmin(v[e], v[e + dd]);
-        v[e] = desc ? hi : lo;
-        v[e + dd] = desc ? lo : hi;
-      }
-    }
-  }
-  eu_store_prefix<T, E>(v, col, pref + j * P2, n, wsum);
+  __syncthreads();
+  eu_scan_offsets(cs, nch, offs);
 }
 
-// EK1 (radix): the same column sort as a CTA-wide LSD radix sort
-// (cub::BlockRadixSort over the |y| bit patterns -- non-negative floats
-// order like their bits; padding 0 sorts last among equals, so the first n
-// sorted keys are the column's), then the same prefix pass.  Blocked
-// arrangement: thread t ends with ranks t*E .. t*E+E-1, as in the bitonic
-// network; sorted values are identical, so is everything downstream.
-template <typename T, int NT, int E>
-__global__ void __launch_bounds__(NT) k_eu_sort_radix(T* __restrict__ mags, DD* __restrict__ pref, int64_t n,
-                                                      const mp_info* __restrict__ info) {
+// Lanes of the warp holding the same 8-bit digit d (d < 256; 256 marks an
+// absent key): one ballot per digit bit, AND-ed per lane -- branch-free,
+// unlike __match_any_sync (the sort ran 1.8 ms with it, serialised).
+__device__ __forceinline__ unsigned eu_peers(int d) {
+  unsigned peers = __ballot_sync(0xffffffffu, d < 256) ;
+  peers = d < 256 ? peers : ~peers;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const unsigned v = __ballot_sync(0xffffffffu, (d >> b) & 1);
+    peers &= ((d >> b) & 1) ? v : ~v;
+  }
+  return peers;
+}
+
+// One CTA sorts `run` keys of column blockIdx.y starting at rank
+// blockIdx.x * run, descending, in place.  LSD radix sort on the |y| bit
+// patterns (non-negative floats order like their bits), 8-bit digits taken
+// complemented so the ascending stable passes give a descending order.
+// Warp w owns the contiguous segment [w * seg, (w + 1) * seg) and walks it
+// 32 keys at a time, so (segment, step, lane) is the array order: per-warp
+// digit histograms -> digit-major, warp-minor exclusive offsets -> scatter at
+// offset + rank among the step's equal digits (eu_peers: the lowest peer
+// updates the counter, so no two lanes touch one counter).  A pass whose
+// digit is the same for every key is the identity and is skipped.  A whole
+// column (gridDim.x == 1) also gets its chunk prefix offsets.
+template <typename T>
+__global__ void __launch_bounds__(kEuSortThreads) k_eu_sort(T* __restrict__ mags, int64_t ld, int64_t n, int64_t run,
+                                                            DD* __restrict__ offs, double* __restrict__ fb,
+                                                            int64_t ldo, const mp_info* __restrict__ info) {
   if (info->status != MP_OK) return;
   using K = typename BitsT<T>::type;
-  using Sort = cub::BlockRadixSort<K, NT, E, cub::NullType, kEuRadixBits>;
-  // CUB's temp storage in dynamic shared memory (above 48 KiB for 1024 threads)
-  extern __shared__ __align__(16) unsigned char eu_radix_smem[];
-  typename Sort::TempStorage& tmp = *reinterpret_cast<typename Sort::TempStorage*>(eu_radix_smem);
-  __shared__ DD wsum[32];
+  constexpr int NT = kEuSortThreads, NW = kEuSortWarps;
+  extern __shared__ __align__(16) unsigned char eu_smem[];
+  int* hist = reinterpret_cast<int*>(eu_smem);  // [NW][256]
+  K* A = reinterpret_cast<K*>(eu_smem + kEuHistBytes);
+  K* B = A + ((run + 3) & ~int64_t(3));  // 16-byte aligned: chunk sums (DD) land there later
+  __shared__ int tot_s[kEuDigits];
+  __shared__ int wsum[8];
+  __shared__ int skip;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t j = blockIdx.y, r0 = static_cast<int64_t>(blockIdx.x) * run;
+  const int len = static_cast<int>(min(run, n - r0));
+  T* col = mags + j * ld + r0;
+  for (int i = tid; i < len; i += NT) A[i] = abs_bits(col[i]);
+  const int seg = ((len + NW * 32 - 1) / (NW * 32)) * 32;
+  const unsigned lt = (1u << lane) - 1u;
+  int* hw = hist + warp * kEuDigits;
+  for (int sh = 0; sh < static_cast<int>(sizeof(K) * 8 - 1); sh += 8) {
+    for (int i = tid; i < NW * kEuDigits; i += NT) hist[i] = 0;
+    if (tid == 0) skip = 0;
+    __syncthreads();
+    for (int st = 0; st < seg; st += 32) {
+      const int i = warp * seg + st + lane;
+      const int d = i < len ? 255 - static_cast<int>((A[i] >> sh) & 255u) : kEuDigits;
+      const unsigned peers = eu_peers(d);
+      if (d < kEuDigits && (peers & lt) == 0u) hw[d] += __popc(peers);
+    }
+    __syncthreads();
+    // exclusive offsets, digit-major then warp (threads 0..255: one digit each)
+    int tot = 0;
+    if (tid < kEuDigits) {
+      for (int w = 0; w < NW; ++w) {
+        const int c = hist[w * kEuDigits + tid];
+        hist[w * kEuDigits + tid] = tot;
+        tot += c;
+      }
+      if (tot == len) skip = 1;  // one digit holds every key: identity pass
+      int inc = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+      }
+      if (lane == 31) wsum[warp] = inc;
+      tot_s[tid] = inc - tot;  // exclusive within the warp
+    }
+    __syncthreads();
+    if (skip) continue;  // uniform: every thread read the same flag
+    if (tid < kEuDigits) {
+      int base = tot_s[tid];
+      for (int w = 0; w < warp; ++w) base += wsum[w];
+      for (int w = 0; w < NW; ++w) hist[w * kEuDigits + tid] += base;
+    }
+    __syncthreads();
+    for (int st = 0; st < seg; st += 32) {
+      const int i = warp * seg + st + lane;
+      const bool ok = i < len;
+      const K key = ok ? A[i] : K(0);
+      const int d = ok ? 255 - static_cast<int>((key >> sh) & 255u) : kEuDigits;
+      const unsigned peers = eu_peers(d);
+      const int rank = __popc(peers & lt);
+      const int base = ok ? hw[d] : 0;
+      __syncwarp();
+      if (ok) {
+        B[base + rank] = key;
+        if (rank == 0) hw[d] = base + __popc(peers);
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    K* t = A;
+    A = B;
+    B = t;
+  }
+  for (int i = tid; i < len; i += NT) {
+    if constexpr (sizeof(T) == 4) col[i] = __uint_as_float(A[i]);
+    else col[i] = __longlong_as_double(static_cast<long long>(A[i]));
+  }
+  if (gridDim.x == 1) {
+    __syncthreads();  // the other key buffer is free: chunk sums live there
+    eu_prefix_offsets([&](int64_t i) { return eu_key_value(A[i]); }, len, reinterpret_cast<DD*>(B),
+                      offs + j * ldo);
+    eu_first_breaks([&](int64_t i) { return eu_key_value(A[i]); }, len, offs + j * ldo, fb + j * ldo);
+  }
+}
+
+// EK1 for columns of up to NT * 16 keys (n <= 16384): the in-CTA sort is
+// cub::BlockRadixSort (4-bit digits, 16 keys per thread; our own LSD kernel
+// above measured 1.8 ms with __match_any_sync ranks and 2.5 ms with ballot
+// ranks on 4096 x 16384, against 0.6 ms here -- it ranks a warp's 32 keys at
+// a time, CUB ranks each thread's 16 keys with private counters).  The sorted
+// blocked keys go through shared memory (one pad word per 32: conflict-free
+// blocked writes) to coalesced column stores and the chunk prefix offsets.
+template <typename T, int NT>
+struct EuBlock {
+  static constexpr int E = 16;
+  using K = typename BitsT<T>::type;
+  using Sort = cub::BlockRadixSort<K, NT, E, cub::NullType, 4>;
+  // CUB's temp storage, then (after the sort) the padded sorted keys in the
+  // same bytes, then the chunk sums
+  static constexpr size_t kKeys = (static_cast<size_t>(NT) * E * 33 / 32 * sizeof(K) + 15) & ~size_t(15);
+  static constexpr size_t kTmp = (sizeof(typename Sort::TempStorage) + 15) & ~size_t(15);
+  static constexpr size_t kUnion = kTmp > kKeys ? kTmp : kKeys;
+  static constexpr size_t kSmem = kUnion + static_cast<size_t>(NT) * E / kEuChunk * sizeof(DD);
+};
+
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) k_eu_sort_block(T* __restrict__ mags, int64_t ld, int64_t n,
+                                                      DD* __restrict__ offs, double* __restrict__ fb, int64_t ldo,
+                                                      const mp_info* __restrict__ info) {
+  if (info->status != MP_OK) return;
+  using Cfg = EuBlock<T, NT>;
+  constexpr int E = Cfg::E;
+  using K = typename Cfg::K;
+  extern __shared__ __align__(16) unsigned char eu_blk_smem[];
+  typename Cfg::Sort::TempStorage& tmp = *reinterpret_cast<typename Cfg::Sort::TempStorage*>(eu_blk_smem);
+  K* S = reinterpret_cast<K*>(eu_blk_smem);  // aliases tmp once the sort is done
+  DD* cs = reinterpret_cast<DD*>(eu_blk_smem + Cfg::kUnion);
   const int tid = threadIdx.x;
   const int64_t j = blockIdx.x;
-  T* col = mags + j * (NT * E);
+  T* col = mags + j * ld;
   K key[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = e * NT + tid;  // striped, coalesced
-    key[e] = i < n ? abs_bits(col[i]) : K(0);
+    key[e] = i < n ? abs_bits(col[i]) : K(0);  // padding: 0 sorts last
   }
-  // magnitudes: the sign bit is always clear, sort the low 31 / 63 bits
-  Sort(tmp).SortDescending(key, 0, static_cast<int>(sizeof(K) * 8 - 1));
-  T v[E];
+  typename Cfg::Sort(tmp).SortDescending(key, 0, static_cast<int>(sizeof(K) * 8 - 1));  // sign bit always clear
+  __syncthreads();  // temp storage dead: reuse it for the keys
+  auto pad = [](int i) { return i + (i >> 5); };
+  // chunk sums straight from the registers: thread t holds ranks 16t ..
+  // 16t + 15 (padding keys are 0), chunk c = threads 2c, 2c + 1
+  DD part{0.0, 0.0};
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    if constexpr (sizeof(T) == 4) v[e] = __uint_as_float(key[e]);
-    else v[e] = __longlong_as_double(static_cast<long long>(key[e]));
+    S[pad(tid * E + e)] = key[e];
+    part = dd_add(part, eu_key_value(key[e]));
   }
-  eu_store_prefix<T, E>(v, col, pref + j * (NT * E), n, wsum);
+  const DD other{__shfl_xor_sync(0xffffffffu, part.hi, 1), __shfl_xor_sync(0xffffffffu, part.lo, 1)};
+  if ((tid & 1) == 0) cs[tid >> 1] = dd_add(part, other);
+  __syncthreads();
+  for (int i = tid; i < n; i += NT) {
+    if constexpr (sizeof(T) == 4) col[i] = __uint_as_float(S[pad(i)]);
+    else col[i] = __longlong_as_double(static_cast<long long>(S[pad(i)]));
+  }
+  eu_scan_offsets(cs, (n + kEuChunk - 1) / kEuChunk, offs + j * ldo);
+  eu_first_breaks([&](int64_t i) { return eu_key_value(S[pad(static_cast<int>(i))]); }, n, offs + j * ldo,
+                  fb + j * ldo);
+}
+
+// EK1b: merge pairs of sorted (descending) runs of width w into dst: each
+// thread finds its output diagonal's split by a binary search (merge path,
+// ties taken from the first run: stable) and merges kEuMergeE outputs.
+template <typename T>
+__global__ void __launch_bounds__(kEuMergeThreads) k_eu_merge(const T* __restrict__ src, T* __restrict__ dst,
+                                                              int64_t ld, int64_t n, int64_t w,
+                                                              const mp_info* __restrict__ info) {
+  if (info->status != MP_OK) return;
+  const int64_t j = blockIdx.y;
+  const T* s = src + j * ld;
+  T* d = dst + j * ld;
+  const int64_t p0 = (static_cast<int64_t>(blockIdx.x) * kEuMergeThreads + threadIdx.x) * kEuMergeE;
+  if (p0 >= n) return;
+  const int64_t lo = (p0 / (2 * w)) * (2 * w);
+  const int64_t la = min(w, n - lo), lb = max(int64_t(0), min(w, n - lo - w));
+  const T* a = s + lo;
+  const T* b = a + la;
+  const int64_t diag = p0 - lo;
+  int64_t ilo = max(int64_t(0), diag - lb), ihi = min(diag, la);
+  while (ilo < ihi) {
+    const int64_t mid = (ilo + ihi) >> 1;
+    if (a[mid] >= b[diag - 1 - mid]) ilo = mid + 1;
+    else ihi = mid;
+  }
+  int64_t i = ilo, k = diag - ilo;
+  const int64_t end = min(p0 + kEuMergeE, lo + la + lb);
+  for (int64_t p = p0; p < end; ++p) {
+    if (i < la && (k >= lb || a[i] >= b[k])) d[p] = a[i++];
+    else d[p] = b[k++];
+  }
+}
+
+// Prefix offsets of merged (long) columns: one CTA per column; the chunk
+// sums are staged in offs itself (the scan reads each before overwriting it).
+template <typename T>
+__global__ void __launch_bounds__(256) k_eu_prefix(const T* __restrict__ mags, int64_t ld, int64_t n,
+                                                   DD* __restrict__ offs, double* __restrict__ fb, int64_t ldo,
+                                                   const mp_info* __restrict__ info) {
+  if (info->status != MP_OK) return;
+  const int64_t j = blockIdx.x;
+  const T* col = mags + j * ld;
+  eu_prefix_offsets([&](int64_t i) { return static_cast<double>(col[i]); }, n, offs + j * ldo, offs + j * ldo);
+  eu_first_breaks([&](int64_t i) { return static_cast<double>(col[i]); }, n, offs + j * ldo, fb + j * ldo);
 }
 
 // ------------------------------------------------------------------- EK2
-__device__ __forceinline__ DD dd_sub(DD a, DD b) { return dd_add(a, DD{-b.hi, -b.lo}); }
 // DD / k for an integer k >= 1
 __device__ __forceinline__ DD dd_div_int(DD a, double k) {
   const double q = a.hi / k;
@@ -296,38 +411,85 @@ __device__ __forceinline__ double dd_div_to_double(DD a, DD b) {
 
 template <typename T>
 struct EuCol {
-  const T* a_;   // sorted magnitudes, descending (EuLayout slots)
-  const DD* P_;  // prefix sums P_k = a_1 + ... + a_k (EuLayout slots)
+  const T* a_;      // sorted magnitudes, descending, rank-contiguous
+  const DD* off;    // off[c] = a_0 + ... + a_{32c-1}
+  const double* fb; // fb[c] = t_{32c+1}, the chunk's first breakpoint
   int64_t n;
-  EuLayout L;
-  __device__ __forceinline__ T a(int64_t r) const { return a_[L.slot(r)]; }     // a_{r+1}
-  __device__ __forceinline__ DD P(int64_t r) const { return P_[L.slot(r)]; }    // P_{r+1}
-  // t_k = P_k - k a_k rounded to double (euclidean.cpp:44-45), k = 1..n
-  __device__ __forceinline__ double brk(int64_t k) const {
-    const DD pk = P(k - 1);
+  __device__ __forceinline__ T a(int64_t r) const { return a_[r]; }  // a_{r+1}
+  // P_{r+1} = a_1 + ... + a_{r+1}: the chunk's offset plus its ranks up to r
+  __device__ __forceinline__ DD P(int64_t r) const {
+    const int64_t c0 = r & ~int64_t(kEuChunk - 1);
+    DD s = off[c0 / kEuChunk];
+    for (int64_t i = c0; i <= r; ++i) s = dd_add(s, static_cast<double>(a_[i]));
+    return s;
+  }
+  __device__ __forceinline__ double brk_from_a(DD pk, int64_t k, double ak) const {  // t_k from P_k, a_k
+    const double kk = static_cast<double>(k);
+    const double p = kk * ak, pe = fma(kk, ak, -p);
+    const DD t = dd_sub(pk, DD{p, pe});
+    return t.hi + t.lo;
+  }
+  __device__ __forceinline__ double brk_from(DD pk, int64_t k) const {  // t_k from P_k
     const double ak = static_cast<double>(a(k - 1)), kk = static_cast<double>(k);
     const double p = kk * ak, pe = fma(kk, ak, -p);
     const DD t = dd_sub(pk, DD{p, pe});
     return t.hi + t.lo;
   }
+  // t_k = P_k - k a_k rounded to double (euclidean.cpp:44-45), k = 1..n
+  __device__ __forceinline__ double brk(int64_t k) const { return brk_from(P(k - 1), k); }
   __device__ __forceinline__ double total() const { const DD t = P(n - 1); return t.hi + t.lo; }
-  // #{k : t_k <= theta} (the breakpoints are non-decreasing)
-  __device__ __forceinline__ int64_t segment(double theta) const {
-    int64_t lo = 0, hi = n;
+  // The linear segment of u(theta) holding theta: k = #{k : t_k <= theta}
+  // (>= 1: t_1 = 0 <= theta), P_k, t_k and the segment's end t_{k+1} (P_n
+  // for k = n).  A binary search over the chunks' first breakpoints (the
+  // breakpoints are non-decreasing), then one walk inside the chunk that
+  // carries P_k along (euclidean.cpp:19-26 bisects all n breakpoints).
+  struct Seg {
+    int64_t k;
+    DD pk;
+    double tk, tk1;
+  };
+  __device__ __forceinline__ Seg segment(double theta) const {
+    const int64_t nch = (n + kEuChunk - 1) / kEuChunk;
+    int64_t lo = 1, hi = nch;  // chunks [0, lo) start at or below theta (chunk 0: t_1 = 0)
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
-      if (brk(mid + 1) <= theta) lo = mid + 1;
+      if (fb[mid] <= theta) lo = mid + 1;
       else hi = mid;
     }
-    return lo;
+    const int64_t k0 = (lo - 1) * kEuChunk + 1;
+    // the chunk's ranks and the next chunk's first, loaded up front (one
+    // line; the walk below would otherwise wait on each load in turn)
+    double v[kEuChunk + 1];
+#pragma unroll
+    for (int i = 0; i <= kEuChunk; ++i) v[i] = k0 - 1 + i < n ? static_cast<double>(a_[k0 - 1 + i]) : 0.0;
+    Seg r{k0, dd_add(off[lo - 1], v[0]), 0.0, 0.0};
+    r.tk = brk_from_a(r.pk, k0, v[0]);
+    r.tk1 = -1.0;
+#pragma unroll
+    for (int i = 1; i <= kEuChunk; ++i) {  // up to the next chunk's first (> theta)
+      const int64_t k = k0 + i;
+      if (k > n) break;
+      const DD pn = dd_add(r.pk, v[i]);
+      const double tn = brk_from_a(pn, k, v[i]);
+      if (tn > theta) {
+        r.tk1 = tn;
+        break;
+      }
+      r.k = k;
+      r.pk = pn;
+      r.tk = tn;
+    }
+    if (r.tk1 < 0.0) r.tk1 = r.k == n ? r.pk.hi + r.pk.lo : brk(r.k + 1);  // k = n: the segment ends at P_n
+    return r;
   }
 };
 
 template <typename T>
 __global__ void __launch_bounds__(kEuSearchThreads)
-    k_eu_search(const T* __restrict__ mags, const DD* __restrict__ pref, int64_t n, int64_t m, EuLayout lay, double eta,
-                double* __restrict__ colmax, double* __restrict__ budgets, mp_info* __restrict__ info,
-                EuScratch* __restrict__ sc) {
+    k_eu_search(const T* __restrict__ mags, const DD* __restrict__ offs, const double* __restrict__ fbs, int64_t n,
+                int64_t m, int64_t ld, int64_t ldo,
+                double eta, double* __restrict__ colmax, double* __restrict__ budgets, double* __restrict__ coltot,
+                mp_info* __restrict__ info, EuScratch* __restrict__ sc) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   if (info->status != MP_OK) return;  // written by EK0 before this launch: uniform
@@ -341,11 +503,13 @@ __global__ void __launch_bounds__(kEuSearchThreads)
   DD l1{0.0, 0.0};
   double tmax = 0.0;
   for (int64_t j = j0; j < m; j += js) {
-    const EuCol<T> c{mags + j * lay.ld, pref + j * lay.ld, n, lay};
+    const EuCol<T> c{mags + j * ld, offs + j * ldo, fbs + j * ldo, n};
     const double a1 = static_cast<double>(c.a(0));
     colmax[j] = a1;
     l1 = dd_add(l1, a1);
-    tmax = fmax(tmax, c.total());
+    const double tot = c.total();
+    coltot[j] = tot;  // P_n, read back by every Newton step
+    tmax = fmax(tmax, tot);
   }
   l1 = block_sum_dd(l1, dscr);
   tmax = -block_min(-tmax, fscr);
@@ -382,16 +546,14 @@ __global__ void __launch_bounds__(kEuSearchThreads)
       DD A{0.0, 0.0}, B{0.0, 0.0};
       double lo = 0.0, hi = __longlong_as_double(0x7ff0000000000000ll);
       for (int64_t j = j0; j < m; j += js) {
-        const EuCol<T> c{mags + j * lay.ld, pref + j * lay.ld, n, lay};
-        const double tot = c.total();
-        if (theta >= tot) continue;  // inactive column
-        int64_t k = c.segment(theta);
-        if (k == 0) k = 1;
-        const double kd = static_cast<double>(k);
-        A = dd_add(A, dd_div_int(c.P(k - 1), kd));
+        if (theta >= coltot[j]) continue;  // inactive column
+        const EuCol<T> c{mags + j * ld, offs + j * ldo, fbs + j * ldo, n};
+        const typename EuCol<T>::Seg g = c.segment(theta);
+        const double kd = static_cast<double>(g.k);
+        A = dd_add(A, dd_div_int(g.pk, kd));
         B = dd_add(B, dd_div_int(DD{1.0, 0.0}, kd));
-        lo = fmax(lo, c.brk(k));
-        hi = fmin(hi, k < n ? c.brk(k + 1) : tot);
+        lo = fmax(lo, g.tk);
+        hi = fmin(hi, g.tk1);
       }
       A = block_sum_dd(A, dscr);
       B = block_sum_dd(B, dscr);
@@ -432,16 +594,15 @@ __global__ void __launch_bounds__(kEuSearchThreads)
   // budgets (euclidean.cpp:143-149)
   long long zc = 0;
   for (int64_t j = j0; j < m; j += js) {
-    const EuCol<T> c{mags + j * lay.ld, pref + j * lay.ld, n, lay};
+    const EuCol<T> c{mags + j * ld, offs + j * ldo, fbs + j * ldo, n};
     double u;
     if (mode == 0) {
       u = static_cast<double>(c.a(0));
-    } else if (mode == 1 || theta >= c.total()) {
+    } else if (mode == 1 || theta >= coltot[j]) {
       u = 0.0;
     } else {
-      int64_t k = c.segment(theta);
-      if (k == 0) k = 1;
-      const DD d = dd_div_int(dd_sub(c.P(k - 1), DD{theta, 0.0}), static_cast<double>(k));
+      const typename EuCol<T>::Seg g = c.segment(theta);
+      const DD d = dd_div_int(dd_sub(g.pk, DD{theta, 0.0}), static_cast<double>(g.k));
       u = fmax(0.0, d.hi + d.lo);
     }
     budgets[j] = u;
