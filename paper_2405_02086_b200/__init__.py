@@ -126,10 +126,11 @@ class BilevelProjector:
         _check_operand(y, "y", (self.n, self.m), self.tdtype, self.device)
         _check_operand(x, "x", (self.n, self.m), self.tdtype, self.device)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        check(lib().mp_bilevel_project(y.data_ptr(), x.data_ptr(), self.dt, self.n, self.m, self.p, self.q,
-                                       float(eta), self.budgets.data_ptr(), self.norms.data_ptr(),
-                                       self.info_buf.data_ptr(), self.flags, self.ws.data_ptr(), self.ws.numel(),
-                                       s.cuda_stream))
+        with torch.cuda.device(self.device):  # the C-ABI launches on the current device
+            check(lib().mp_bilevel_project(y.data_ptr(), x.data_ptr(), self.dt, self.n, self.m, self.p, self.q,
+                                           float(eta), self.budgets.data_ptr(), self.norms.data_ptr(),
+                                           self.info_buf.data_ptr(), self.flags, self.ws.data_ptr(),
+                                           self.ws.numel(), s.cuda_stream))
         return x
 
     def info(self) -> MpInfo:
@@ -168,11 +169,12 @@ class MultilevelProjector:
         _check_operand(t, "t", self.shape, self.tdtype, self.device)
         _check_operand(x, "x", self.shape, self.tdtype, self.device)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        check(lib().mp_multilevel_project(t.data_ptr(), x.data_ptr(), self.dt, self._shape_c, len(self.shape),
-                                          self._lv_c, len(self.levels), float(eta),
-                                          self.chain.data_ptr() if self.want_chain else None,
-                                          self.info_buf.data_ptr(), self.flags, self.ws.data_ptr(),
-                                          self.ws.numel(), s.cuda_stream))
+        with torch.cuda.device(self.device):
+            check(lib().mp_multilevel_project(t.data_ptr(), x.data_ptr(), self.dt, self._shape_c, len(self.shape),
+                                              self._lv_c, len(self.levels), float(eta),
+                                              self.chain.data_ptr() if self.want_chain else None,
+                                              self.info_buf.data_ptr(), self.flags, self.ws.data_ptr(),
+                                              self.ws.numel(), s.cuda_stream))
         return x
 
     def budget_chain(self):
@@ -372,8 +374,9 @@ def euclid_project_l1inf(y, eta):
         budgets = torch.empty(m, dtype=torch.float64, device=yc.device)
         info = torch.zeros(C.sizeof(MpInfo), dtype=torch.uint8, device=yc.device)
         s = torch.cuda.current_stream(yc.device)
-        check(lib().mp_euclid_project(yc.data_ptr(), x.data_ptr(), dt, n, m, float(eta), budgets.data_ptr(),
-                                      info.data_ptr(), 0, ws.data_ptr(), wsb, s.cuda_stream))
+        with torch.cuda.device(yc.device):
+            check(lib().mp_euclid_project(yc.data_ptr(), x.data_ptr(), dt, n, m, float(eta), budgets.data_ptr(),
+                                          info.data_ptr(), 0, ws.data_ptr(), wsb, s.cuda_stream))
         inf = MpInfo.from_buffer_copy(info.cpu().numpy().tobytes())
         check(inf.status)
         return x, budgets, float(inf.tau)
@@ -396,8 +399,9 @@ def perturb_gaussian(x, sigma, seed, iteration, stream=None):
     if not _is_cuda_tensor(x) or not x.is_contiguous():
         raise MpConfigError("perturb_gaussian needs a contiguous CUDA tensor")
     s = stream if stream is not None else torch.cuda.current_stream(x.device)
-    check(lib().mp_perturb_gaussian(x.data_ptr(), _dt(x), x.numel(), float(sigma), int(seed), int(iteration),
-                                    s.cuda_stream))
+    with torch.cuda.device(x.device):
+        check(lib().mp_perturb_gaussian(x.data_ptr(), _dt(x), x.numel(), float(sigma), int(seed), int(iteration),
+                                        s.cuda_stream))
     return x
 
 

@@ -59,6 +59,7 @@ class CudaBackend:
         self.info = t.zeros(C.sizeof(_capi.MpInfo), dtype=t.uint8, device=self.device)
 
     def _stream(self):
+        self.torch.cuda.set_device(self.device)  # the C-ABI launches on the current device
         return self.torch.cuda.current_stream(self.device).cuda_stream
 
     def norms(self, y_local, q: int, out):

@@ -109,3 +109,23 @@ def test_multilevel_euclid_fibers_in_bounds():
 def O_norms(y, q):
     a = np.abs(y.astype(np.float64))
     return a.sum(0) if q == 0 else (np.sqrt((a * a).sum(0)) if q == 1 else a.max(0))
+
+
+def test_kernel_attributes_per_device():
+    """Function attributes (large dynamic shared memory, non-portable
+    clusters) are set per device: the TMA strips, the cluster K2 and the
+    euclid sort must launch on a second device of the same process."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs in one process")
+    rng = np.random.default_rng(8)
+    y_h = rng.normal(size=(3000, 16384)).astype(np.float32)  # 256-thread TMA strips, 16-CTA cluster K2
+    eta = 0.05 * float(np.abs(y_h.astype(np.float64)).sum())
+    outs = []
+    for dev in (0, 1):
+        y = torch.from_numpy(y_h).to(f"cuda:{dev}")
+        x, b, z = mp.bilevel_project(y, eta, "1", "1")
+        xe, be, th = mp.euclid_project_l1inf(y[:, :64].contiguous(), 5.0)
+        torch.cuda.synchronize(dev)
+        outs.append((x.cpu().numpy(), xe.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
