@@ -787,8 +787,9 @@ mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, doubl
   prof_mark(0, s);
   MP_CUDA_TRY(cudaMemsetAsync(inf, 0, sizeof(mp_info), s));
   T* mags = static_cast<T*>(w.mags);
-  mpk::k_eu_gather<T><<<dim3(static_cast<unsigned>((m + 31) / 32), static_cast<unsigned>((n + 31) / 32)), dim3(32, 8),
-                        0, s>>>(y, n, m, mags, w.ld, inf);
+  mpk::k_eu_gather<T><<<dim3(static_cast<unsigned>((m + mpk::kEuTile - 1) / mpk::kEuTile),
+                           static_cast<unsigned>((n + mpk::kEuTile - 1) / mpk::kEuTile)),
+                      dim3(32, 8), 0, s>>>(y, n, m, mags, w.ld, inf);
   MP_CUDA_TRY(cudaGetLastError());
   static std::atomic<uint64_t> done{0};
   MP_CUDA_TRY(mpi::once_per_device(done, [] {

@@ -69,28 +69,38 @@ struct EuScratch {
 };
 
 // ------------------------------------------------------------------- EK0
+// 64 x 64 tiles, 256 threads, 16 elements per thread (32 x 32 tiles of 4
+// per thread ran 121 us on 4096 x 16384, 68% of HBM: the grid was 65536 CTAs
+// of little work each).
+constexpr int kEuTile = 64;
 template <typename T>
 __global__ void __launch_bounds__(256) k_eu_gather(const T* __restrict__ y, int64_t n, int64_t m, T* __restrict__ mags,
                                                    int64_t ld, mp_info* __restrict__ info) {
-  __shared__ T tile[32][33];
-  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32, r0 = static_cast<int64_t>(blockIdx.y) * 32;
+  __shared__ T tile[kEuTile][kEuTile + 1];
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kEuTile, r0 = static_cast<int64_t>(blockIdx.y) * kEuTile;
   const int tx = threadIdx.x, ty = threadIdx.y;  // (32, 8)
   bool bad = false;
 #pragma unroll
-  for (int k = 0; k < 32; k += 8) {
-    const int64_t r = r0 + ty + k, c = c0 + tx;
-    T e = T(0);
-    if (r < n && c < m) {
-      e = y[r * m + c];
-      bad |= !isfinite(e);
+  for (int k = 0; k < kEuTile; k += 8) {
+#pragma unroll
+    for (int h = 0; h < kEuTile; h += 32) {
+      const int64_t r = r0 + ty + k, c = c0 + tx + h;
+      T e = T(0);
+      if (r < n && c < m) {
+        e = y[r * m + c];
+        bad |= !isfinite(e);
+      }
+      tile[ty + k][tx + h] = fabs(e);
     }
-    tile[ty + k][tx] = fabs(e);
   }
   if (__syncthreads_or(bad) && tx == 0 && ty == 0) info->status = MP_ERR_VALUE;
 #pragma unroll
-  for (int k = 0; k < 32; k += 8) {
-    const int64_t c = c0 + ty + k, r = r0 + tx;
-    if (r < n && c < m) mags[c * ld + r] = tile[tx][ty + k];
+  for (int k = 0; k < kEuTile; k += 8) {
+#pragma unroll
+    for (int h = 0; h < kEuTile; h += 32) {
+      const int64_t c = c0 + ty + k, r = r0 + tx + h;
+      if (r < n && c < m) mags[c * ld + r] = tile[tx + h][ty + k];
+    }
   }
 }
 
