@@ -47,6 +47,13 @@
 #include "mp_kernels.cuh"
 #include "mp_l1cols.cuh"
 
+#ifndef MP_L1_DYNAMIC
+#define MP_L1_DYNAMIC 1
+#endif
+#ifndef MP_L1_DELAY_NS
+#define MP_L1_DELAY_NS 0
+#endif
+
 namespace mpk {
 
 constexpr int kRegRPT = 16;       // 16-byte row pieces per thread
@@ -239,6 +246,14 @@ __device__ __forceinline__ float halfnormal_tau(double v, double u, int n) {
   return fmaf(r - static_cast<float>(k), z1 - z0, z0) * sig;
 }
 
+// Compiler barrier that keeps four pieces live in distinct registers.
+__device__ __forceinline__ void pin_regs(uint4& a, uint4& b, uint4& c, uint4& d) {
+  asm volatile("" : "+r"(a.x), "+r"(a.y), "+r"(a.z), "+r"(a.w), "+r"(b.x), "+r"(b.y), "+r"(b.z), "+r"(b.w),
+                    "+r"(c.x), "+r"(c.y), "+r"(c.z), "+r"(c.w), "+r"(d.x), "+r"(d.y), "+r"(d.z), "+r"(d.w)
+               :
+               : "memory");
+}
+
 template <typename T, int P, bool DERIVE, bool PERSIST, int NT = kRegThreads, int RS = 0, bool TMA = false>
 __global__ void __launch_bounds__(NT, kRegThreads / NT)
     k_l1reg(const T* __restrict__ y, T* __restrict__ x, int n, int64_t m, const double* __restrict__ v,
@@ -314,6 +329,12 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
     return;
   }
 
+#if MP_L1_DELAY_NS > 0
+  if (blockIdx.x >= gridDim.x / 2) {  // experiment: de-phase the second CTA of every SM
+    const unsigned long long t0 = gtimer();
+    while (gtimer() - t0 < MP_L1_DELAY_NS) __nanosleep(200);
+  }
+#endif
   auto piece = [&](int i) -> uint4 {  // i is a compile-time index after unrolling
     if (RS == 0 || i < RPT) return q[i < RPT ? i : 0];
     return sq[(i - RPT) * NT + tid];
@@ -324,8 +345,21 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
   __shared__ RegPart<T> wx[2][NW][W];
   const double inv_n = 1.0 / static_cast<double>(n);
   int npass = 0, nx = 0, nst = 0;
+#ifdef MP_L1_CYCLES  // profiling build: per-phase SM cycles of thread 0 (slots 12..15)
+  long long cyw = 0, cyp = 0, cya = 0, cyx = 0;
+#endif
+  // Strips after the first are claimed from a counter K2 zeroed
+  // (OuterParams::next_strip): an SM that streams faster takes more strips.
+  // With the static stride the slowest CTA ended ~19 us after the mean
+  // (config 3).  Claimed at the top of a strip, used at its apply.
+  constexpr bool kDyn = DERIVE && PERSIST && MP_L1_DYNAMIC;
+  __shared__ unsigned s_next[2];
   for (;;) {
     ++nst;
+    if constexpr (kDyn) {
+      if (tid == 0)
+        s_next[nst & 1] = gridDim.x + atomicAdd(&const_cast<OuterParams*>(params)->next_strip, 1u);
+    }
     const int64_t cb = strip * W + pc;
     // strip column `lane` (< W): iteration state, identical in every warp;
     // the threads' own columns (pc .. pc + C4 - 1) come from these lanes by
@@ -359,6 +393,9 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
       livem |= (kd == 3u ? 1u : 0u) << c;
       thr[c] = __shfl_sync(0xffffffffu, t1, pc + c);
     }
+#ifdef MP_L1_CYCLES
+    const long long ck0 = clock64();
+#endif
     const bool any_proj = __any_sync(0xffffffffu, pj);
     if constexpr (TMA) {
       mbar_wait(&mbar, mph);
@@ -367,6 +404,9 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
 
+#ifdef MP_L1_CYCLES
+    const long long ck1 = clock64();
+#endif
     if (any_proj) {
       bool xp = false;  // exact pass (CTA-uniform)
       for (int par = 0, it = 0; it < 4 * 1024; par ^= 1, ++it) {
@@ -497,16 +537,19 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
         xp = xp || __ballot_sync(0xffffffffu, lv && ex) != 0u;
       }
     }
+#ifdef MP_L1_CYCLES
+    const long long ck2 = clock64();
+#endif
     if (warp == 0 && lane < W) tau_out[strip * W + lane] = pj ? td : -1.0;
 
     // ---- apply from registers
     bool need_store = any_proj || x != y;
 #pragma unroll
     for (int c = 0; c < C4; ++c) need_store = need_store || ((kinds >> (2 * c)) & 3u) == 2u;
-    need_store = __syncthreads_or(need_store);
+    need_store = __syncthreads_or(need_store);  // (also publishes s_next)
     // PERSIST: stream the next strip into each register right after its
     // store, so its loads overlap this strip's apply
-    const int64_t next = strip + gridDim.x;
+    const int64_t next = kDyn ? static_cast<int64_t>(s_next[nst & 1]) : strip + gridDim.x;
     const bool more = PERSIST && next < nstrips;
     // One branch-free rule for every column kind: d = (|y| - tau_hi) - tau_lo;
     // x = d > 0 ? copysign(d, y) : (y & keep).  Feasible columns: tau = 0 and
@@ -532,30 +575,77 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
     }
     T* xq = x + static_cast<int64_t>(rb) * m + cb;
     const T* yn = y + static_cast<int64_t>(rb) * m + next * W + pc;
+    auto shrink = [&](const uint4& qv) -> uint4 {
+      T e[C4];
+      reg_unpack<T>(qv, e);
 #pragma unroll
-    for (int i = 0; i < NPC; ++i, xq += step, yn += step) {
-      if (rb + SL * i >= n) break;
-      if (need_store) {
-        T e[C4];
-        reg_unpack<T>(piece(i), e);
-#pragma unroll
-        for (int c = 0; c < C4; ++c) {
-          if constexpr (kF32) {
-            const float dm = shrink_mag(fabsf(e[c]), TauPair{th_hi[c], th_lo[c]});
-            e[c] = dm > 0.0f ? copysignf(dm, e[c]) : __uint_as_float(__float_as_uint(e[c]) & keep[c]);
-          } else {
-            const double dm = fabs(e[c]) - th_hi[c];
-            e[c] = dm > 0.0 ? copysign(dm, e[c])
-                            : __longlong_as_double(static_cast<long long>(
-                                  static_cast<UT>(__double_as_longlong(e[c])) & keep[c]));
-          }
+      for (int c = 0; c < C4; ++c) {
+        if constexpr (kF32) {
+          const float dm = shrink_mag(fabsf(e[c]), TauPair{th_hi[c], th_lo[c]});
+          e[c] = dm > 0.0f ? copysignf(dm, e[c]) : __uint_as_float(__float_as_uint(e[c]) & keep[c]);
+        } else {
+          const double dm = fabs(e[c]) - th_hi[c];
+          e[c] = dm > 0.0 ? copysign(dm, e[c])
+                          : __longlong_as_double(static_cast<long long>(
+                                static_cast<UT>(__double_as_longlong(e[c])) & keep[c]));
         }
-        if (TMA && i >= RPT) sq[(i >= RPT ? i - RPT : 0) * NT + tid] = reg_pack<T>(e);  // TMA stores it
-        else __stcs(reinterpret_cast<uint4*>(xq), reg_pack<T>(e));
+      }
+      return reg_pack<T>(e);
+    };
+    // the register pieces of a TMA strip: rewritten in place, stored back to
+    // back from their own registers, then the next strip's loaded over them
+    auto reg_pieces = [&]() {
+      if (need_store) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i)
+          if (rb + SL * i < n) q[i] = shrink(q[i]);
+        // all results live at once, each in its own registers (the compiler
+        // would stage every piece through the same four otherwise)
+        static_assert(!TMA || RPT <= 8, "pin_regs: up to eight pieces");
+        pin_regs(q[0], q[1 % RPT], q[2 % RPT], q[3 % RPT]);
+        if constexpr (RPT > 4) pin_regs(q[4 % RPT], q[5 % RPT], q[6 % RPT], q[7 % RPT]);
+        pin_regs(q[0], q[1 % RPT], q[2 % RPT], q[3 % RPT]);
+#pragma unroll
+        for (int i = 0; i < RPT; ++i)
+          if (rb + SL * i < n) __stcs(reinterpret_cast<uint4*>(xq + static_cast<int64_t>(i) * step), q[i]);
       }
       if (more) {
-        if (i < RPT) q[i < RPT ? i : 0] = __ldg(reinterpret_cast<const uint4*>(yn));
-        else if constexpr (RS > 0 && !TMA) cp_async_16(&sq[(i - RPT) * NT + tid], yn);
+#pragma unroll
+        for (int i = 0; i < RPT; ++i)
+          if (rb + SL * i < n) q[i] = __ldg(reinterpret_cast<const uint4*>(yn + static_cast<int64_t>(i) * step));
+      }
+    };
+    // 256- and 512-thread strips (64 / 128 threads measured 1-2% slower)
+    constexpr bool kSplit = TMA && NT >= 256;
+    if constexpr (kSplit) {
+      // A global store holds its source registers for hundreds of cycles while
+      // the memory system is busy with the strips' TMA traffic (ncu: ~800
+      // cycles of long-scoreboard stall on the next write to them, six times
+      // per strip), and fence.proxy.async waits for the stores in flight.  So
+      // the shared-memory pieces go first and their TMA stores are issued
+      // before the register pieces touch global memory.
+      if (need_store) {
+#pragma unroll
+        for (int i = RPT; i < NPC; ++i) {
+          if (rb + SL * i >= n) break;
+          sq[(i - RPT) * NT + tid] = shrink(sq[(i - RPT) * NT + tid]);  // TMA stores it
+        }
+      }
+    } else {
+      // (register-only strips measured 5-20% slower with the split order:
+      // their next strip's loads would start only after all the stores)
+#pragma unroll
+      for (int i = 0; i < NPC; ++i, xq += step, yn += step) {
+        if (rb + SL * i >= n) break;
+        if (need_store) {
+          const uint4 r = shrink(piece(i));
+          if (TMA && i >= RPT) sq[(i >= RPT ? i - RPT : 0) * NT + tid] = r;  // TMA stores it
+          else __stcs(reinterpret_cast<uint4*>(xq), r);
+        }
+        if (more) {
+          if (i < RPT) q[i < RPT ? i : 0] = __ldg(reinterpret_cast<const uint4*>(yn));
+          else if constexpr (RS > 0 && !TMA) cp_async_16(&sq[(i - RPT) * NT + tid], yn);
+        }
       }
     }
     if constexpr (TMA) {
@@ -563,29 +653,32 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
       // the next strip's half lands in the same buffer
       if (need_store) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
-      if (tid == 0) {
-        // up to four store groups: each group's boxes reload as soon as the
-        // engine has read them, while the later groups are still being read
-        // (one group: 179 us on config 3, two or four: 173 us).  Group g is
-        // boxes [g * kBoxes / kG, (g + 1) * kBoxes / kG); 64-thread strips
-        // have three boxes, hence three groups.
-        constexpr int kG = kBoxes < 4 ? kBoxes : 4;
-        static_assert(kG >= 1, "TMA strips: at least one box");
-        auto store = [&](int b0, int b1) {
-          for (int b = b0; b < b1; ++b)
+#ifdef MP_L1_CYCLES
+      cyx += clock64() - ck2;
+#endif
+      // up to four store groups: each group's boxes reload as soon as the
+      // engine has read them, while the later groups are still being read
+      // (one group: 179 us on config 3, two or four: 173 us).  Group g is
+      // boxes [g * kBoxes / kG, (g + 1) * kBoxes / kG); 64-thread strips
+      // have three boxes, hence three groups.
+      constexpr int kG = kBoxes < 4 ? kBoxes : 4;
+      static_assert(kG >= 1, "TMA strips: at least one box");
+      if (tid == 0 && need_store) {
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+          for (int b = g * kBoxes / kG; b < (g + 1) * kBoxes / kG; ++b)
             tma_store_2d(&tm.x, static_cast<int>(strip * W), SL * RPT + b * kBoxRows,
                          reinterpret_cast<const char*>(sq) + b * kBoxRows * W * sizeof(T));
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        };
+        }
+      }
+      if constexpr (kSplit) reg_pieces();
+      if (tid == 0) {
         auto load = [&](int b0, int b1) {
           for (int b = b0; b < b1; ++b)
             tma_load_2d(reinterpret_cast<char*>(sq) + b * kBoxRows * W * sizeof(T), &tm.y,
                         static_cast<int>(next * W), SL * RPT + b * kBoxRows, &mbar);
         };
-        if (need_store) {
-#pragma unroll
-          for (int g = 0; g < kG; ++g) store(g * kBoxes / kG, (g + 1) * kBoxes / kG);
-        }
         if (more) mbar_expect(&mbar, static_cast<unsigned>(RS * NT * 16));
 #pragma unroll
         for (int g = 0; g < kG; ++g) {
@@ -608,6 +701,14 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
         asm volatile("cp.async.commit_group;" ::: "memory");
       }
     }
+#ifdef MP_L1_CYCLES
+    {
+      const long long ck3 = clock64();
+      cyw += ck1 - ck0;
+      cyp += ck2 - ck1;
+      cya += ck3 - ck2;
+    }
+#endif
     if (!more) break;
     strip = next;
   }
@@ -616,6 +717,12 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
     atomicAdd(g_mp_timeline + 11, static_cast<unsigned long long>(nx));
     atomicMax(g_mp_timeline + 9, static_cast<unsigned long long>(npass));
     atomicAdd(g_mp_timeline + 10, static_cast<unsigned long long>(nst));
+#ifdef MP_L1_CYCLES
+    atomicAdd(g_mp_timeline + 12, static_cast<unsigned long long>(cyw));
+    atomicAdd(g_mp_timeline + 13, static_cast<unsigned long long>(cyp));
+    atomicAdd(g_mp_timeline + 14, static_cast<unsigned long long>(cya));
+    atomicAdd(g_mp_timeline + 15, static_cast<unsigned long long>(cyx));
+#endif
   }
   if constexpr (TMA) {
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete

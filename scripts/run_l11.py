@@ -7,7 +7,10 @@ import numpy as np
 import torch
 
 import paper_2405_02086_b200 as mp
-from paper_2405_02086_b200 import datagen
+from paper_2405_02086_b200 import _build, datagen
+
+if os.environ.get("MP_B200_LIB"):
+    _build.LIB = os.environ["MP_B200_LIB"]
 
 q = os.environ.get("Q", "1")
 y_h = datagen.config_input(3)

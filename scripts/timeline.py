@@ -8,7 +8,10 @@ import numpy as np
 import torch
 
 import paper_2405_02086_b200 as mp
-from paper_2405_02086_b200 import _capi, datagen
+from paper_2405_02086_b200 import _build, _capi, datagen
+
+if os.environ.get("MP_B200_LIB"):  # A/B runs: a variant build (scripts/ab_build.sh)
+    _build.LIB = os.environ["MP_B200_LIB"]
 
 L = _capi.lib()
 torch.cuda.set_device(0)
@@ -57,7 +60,7 @@ for rel in [float(r) for r in os.environ.get("RELS", "0.001,0.5").split(",")]:
         if tot > 0:
             print(f"  l1 CTA cycles: wait-for-strip {extra[4] / tot:.1%}  passes {extra[5] / tot:.1%}  "
                   f"apply {extra[6] / tot:.1%}  (per strip: {extra[4] / extra[2]:.0f} / {extra[5] / extra[2]:.0f} / "
-                  f"{extra[6] / extra[2]:.0f} cycles)")
+                  f"{extra[6] / extra[2]:.0f} cycles; apply until the stores are issued {extra[7] / extra[2]:.0f})")
     inf_ = p.info()
     print(f"  info: iterations={inf_.iterations} survivors={inf_.survivors} zero_columns={inf_.zero_columns}")
     r = np.median(np.array(res), axis=0)
