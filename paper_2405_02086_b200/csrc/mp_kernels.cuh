@@ -428,7 +428,7 @@ __device__ __forceinline__ long long block_count(long long c, long long* scr) {
 // norm: u = derive_u(P, v).  Written by K2, read by the apply kernels.
 struct OuterParams {
   int mode;      // 0 identity, 1 zero, 2 l1 threshold tau, 3 l2 scale, 4 linf clip at eta
-  unsigned next_strip;  // work counter of the l1 apply's strips (K2 zeroes it)
+  int pad;
   double tau, scale, eta;
 };
 
@@ -492,7 +492,6 @@ __device__ __forceinline__ double outer_load_fold(const OuterArgs& a, int64_t i)
 __device__ __forceinline__ void outer_publish(const OuterArgs& a, int mode, double tau, double scale) {
   if (a.params) {
     a.params->mode = mode;
-    a.params->next_strip = 0u;
     a.params->tau = tau;
     a.params->scale = scale;
     a.params->eta = a.eta;

@@ -47,13 +47,6 @@
 #include "mp_kernels.cuh"
 #include "mp_l1cols.cuh"
 
-#ifndef MP_L1_DYNAMIC
-#define MP_L1_DYNAMIC 1
-#endif
-#ifndef MP_L1_DELAY_NS
-#define MP_L1_DELAY_NS 0
-#endif
-
 namespace mpk {
 
 constexpr int kRegRPT = 16;       // 16-byte row pieces per thread
@@ -329,12 +322,6 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
     return;
   }
 
-#if MP_L1_DELAY_NS > 0
-  if (blockIdx.x >= gridDim.x / 2) {  // experiment: de-phase the second CTA of every SM
-    const unsigned long long t0 = gtimer();
-    while (gtimer() - t0 < MP_L1_DELAY_NS) __nanosleep(200);
-  }
-#endif
   auto piece = [&](int i) -> uint4 {  // i is a compile-time index after unrolling
     if (RS == 0 || i < RPT) return q[i < RPT ? i : 0];
     return sq[(i - RPT) * NT + tid];
@@ -348,18 +335,11 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
 #ifdef MP_L1_CYCLES  // profiling build: per-phase SM cycles of thread 0 (slots 12..15)
   long long cyw = 0, cyp = 0, cya = 0, cyx = 0;
 #endif
-  // Strips after the first are claimed from a counter K2 zeroed
-  // (OuterParams::next_strip): an SM that streams faster takes more strips.
-  // With the static stride the slowest CTA ended ~19 us after the mean
-  // (config 3).  Claimed at the top of a strip, used at its apply.
-  constexpr bool kDyn = DERIVE && PERSIST && MP_L1_DYNAMIC;
-  __shared__ unsigned s_next[2];
+  // (Strips claimed from a global counter instead of the static stride:
+  // 143 vs 137.6 us on config 3 -- with the stride, neighbouring strips are
+  // in flight together and share the 256-byte L2 promotions of their rows.)
   for (;;) {
     ++nst;
-    if constexpr (kDyn) {
-      if (tid == 0)
-        s_next[nst & 1] = gridDim.x + atomicAdd(&const_cast<OuterParams*>(params)->next_strip, 1u);
-    }
     const int64_t cb = strip * W + pc;
     // strip column `lane` (< W): iteration state, identical in every warp;
     // the threads' own columns (pc .. pc + C4 - 1) come from these lanes by
@@ -546,10 +526,10 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
     bool need_store = any_proj || x != y;
 #pragma unroll
     for (int c = 0; c < C4; ++c) need_store = need_store || ((kinds >> (2 * c)) & 3u) == 2u;
-    need_store = __syncthreads_or(need_store);  // (also publishes s_next)
+    need_store = __syncthreads_or(need_store);
     // PERSIST: stream the next strip into each register right after its
     // store, so its loads overlap this strip's apply
-    const int64_t next = kDyn ? static_cast<int64_t>(s_next[nst & 1]) : strip + gridDim.x;
+    const int64_t next = strip + gridDim.x;
     const bool more = PERSIST && next < nstrips;
     // One branch-free rule for every column kind: d = (|y| - tau_hi) - tau_lo;
     // x = d > 0 ? copysign(d, y) : (y & keep).  Feasible columns: tau = 0 and
