@@ -364,13 +364,12 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
       }
       if (DERIVE && u_out && warp == 0) u_out[strip * W + lane] = ul;
     }
-    unsigned kinds = 0, livem = 0;
+    unsigned kinds = 0;
     T thr[C4];
 #pragma unroll
     for (int c = 0; c < C4; ++c) {
       const unsigned kd = __shfl_sync(0xffffffffu, kdl, pc + c);
       kinds |= kd << (2 * c);
-      livem |= (kd == 3u ? 1u : 0u) << c;
       thr[c] = __shfl_sync(0xffffffffu, t1, pc + c);
     }
 #ifdef MP_L1_CYCLES
@@ -401,7 +400,7 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
 #pragma unroll
           for (int c = 0; c < C4; ++c) {
             a[c] = {AccT(0), 0.0f};
-            th[c] = (livem >> c) & 1u ? thr[c] : T(INFINITY);
+            th[c] = thr[c];  // +inf for columns that are not (or no longer) projected
           }
 #pragma unroll
           for (int i = 0; i < NPC; ++i) {
@@ -424,7 +423,7 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
 #pragma unroll
           for (int c = 0; c < C4; ++c) {
             a[c] = {0.0, 0, T(INFINITY)};
-            th[c] = (livem >> c) & 1u ? thr[c] : T(INFINITY);
+            th[c] = thr[c];  // +inf for columns that are not (or no longer) projected
           }
 #pragma unroll
           for (int i = 0; i < NPC; ++i) {
@@ -448,9 +447,17 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
           // column totals over the warps, in warp order
           RegPart<T> tot;
           if (xp) {
-            tot = wx[par][0][lane];
+            // a fixed pairwise tree (log2 NW dependent f64 adds instead of
+            // NW - 1: the epilogue of a pass is a latency chain)
+            RegPart<T> tw[NW];
 #pragma unroll
-            for (int w = 1; w < NW; ++w) tot = rp_add(tot, wx[par][w][lane]);
+            for (int w = 0; w < NW; ++w) tw[w] = wx[par][w][lane];
+#pragma unroll
+            for (int o = 1; o < NW; o <<= 1) {
+#pragma unroll
+              for (int w = 0; w + o < NW; w += 2 * o) tw[w] = rp_add(tw[w], tw[w + o]);
+            }
+            tot = tw[0];
           } else {
             AccT s32 = AccT(0);  // f32: <= NPC + 5 + NW f32 terms per sum
             float k32 = 0.0f;
@@ -508,11 +515,10 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
             kp = tot.k;
           }
         }
-        const T tl = round_down_to(T(0), td);
+        const T tl = lv ? round_down_to(T(0), td) : T(INFINITY);
 #pragma unroll
         for (int c = 0; c < C4; ++c) thr[c] = __shfl_sync(0xffffffffu, tl, pc + c);
         const unsigned lvb = __ballot_sync(0xffffffffu, lv);
-        livem = (lvb >> pc) & ((1u << C4) - 1u);
         if (lvb == 0u) break;
         xp = xp || __ballot_sync(0xffffffffu, lv && ex) != 0u;
       }
