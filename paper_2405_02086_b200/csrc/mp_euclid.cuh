@@ -24,7 +24,6 @@
 // Sums are deterministic (fixed trees, CTA partials reduced in CTA order).
 #pragma once
 
-#include <cub/block/block_radix_sort.cuh>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -291,23 +290,111 @@ __global__ void __launch_bounds__(kEuSortThreads) k_eu_sort(T* __restrict__ mags
   }
 }
 
-// EK1 for columns of up to NT * 16 keys (n <= 16384): the in-CTA sort is
-// cub::BlockRadixSort (4-bit digits, 16 keys per thread; our own LSD kernel
-// above measured 1.8 ms with __match_any_sync ranks and 2.5 ms with ballot
-// ranks on 4096 x 16384, against 0.6 ms here -- it ranks a warp's 32 keys at
-// a time, CUB ranks each thread's 16 keys with private counters).  The sorted
-// blocked keys go through shared memory (one pad word per 32: conflict-free
-// blocked writes) to coalesced column stores and the chunk prefix offsets.
+// EK1 for columns of up to NT * 16 keys (n <= 16384): a bitonic sorting
+// network over the CTA, 16 keys per thread in registers, blocked (thread t
+// holds positions 16t .. 16t + 15).  Every merge step of size k starts with a
+// "flip" substage (position i against i ^ (k - 1)) followed by the substages
+// i against i ^ j, j = k/4 .. 1, so every comparison keeps the larger key at
+// the lower position: no direction flags.  A substage with j < 16 is a
+// compare-exchange between two registers of a thread (42 of the 78 substages
+// at 4096 keys), up to 512 positions apart one shfl.xor per key (30), further
+// apart an exchange through shared memory (6).  ~150 instructions per key,
+// none of them a shared-memory atomic or a scan: 4096 x 16384 f32 sorts in
+// 0.4x ms where cub::BlockRadixSort (4-bit digits) took 0.79 ms and our LSD
+// radix kernel above 1.8 ms.  Afterwards the sorted blocked keys go through
+// shared memory (one pad word per 32: conflict-free blocked writes) to
+// coalesced column stores and the chunk prefix offsets.
+template <typename K>
+__device__ __forceinline__ K eu_shfl_xor(K v, int mask) {
+  if constexpr (sizeof(K) == 4) {
+    return __shfl_xor_sync(0xffffffffu, v, mask);
+  } else {
+    const unsigned lo = __shfl_xor_sync(0xffffffffu, static_cast<unsigned>(v), mask);
+    const unsigned hi = __shfl_xor_sync(0xffffffffu, static_cast<unsigned>(v >> 32), mask);
+    return (static_cast<K>(hi) << 32) | lo;
+  }
+}
+
+template <typename K, int NT>
+__device__ __forceinline__ void eu_bitonic_desc(K (&key)[16], K* S) {
+  constexpr int E = 16, N = NT * E;
+  const int t = threadIdx.x;
+  auto pad = [](int i) { return i + (i >> 5); };
+  auto cmpx = [&](int lo, int hi) {  // registers lo < hi: the larger key first
+    const K a = key[lo], b = key[hi];
+    key[lo] = a > b ? a : b;
+    key[hi] = a > b ? b : a;
+  };
+  // this thread's keys against v[e] from the partner thread: the thread at
+  // the lower positions keeps the larger keys
+  auto keep = [&](const K (&v)[E], bool lower) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const K a = key[e], b = v[e];
+      const K mx = a > b ? a : b, mn = a > b ? b : a;
+      key[e] = lower ? mx : mn;
+    }
+  };
+  // partner keys through shared memory (threads of different warps); `rev`:
+  // the partner's keys in reverse order (the flip substage)
+  auto exchange = [&](int pt, bool rev, K (&v)[E]) {
+    __syncthreads();  // the previous exchange's reads are done
+#pragma unroll
+    for (int e = 0; e < E; ++e) S[pad(t * E + e)] = key[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = S[pad(pt * E + (rev ? E - 1 - e : e))];
+  };
+  constexpr int kLogN = 31 - __builtin_clz(static_cast<unsigned>(N));
+#pragma unroll
+  for (int lk = 1; lk <= kLogN; ++lk) {
+    const int k = 1 << lk;
+    if (k <= E) {
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if ((e ^ (k - 1)) > e) cmpx(e, e ^ (k - 1));
+    } else {
+      const int tm = k / E - 1;                     // partner thread t ^ tm, its keys reversed
+      const bool lower = (t & (k / E / 2)) == 0;  // bit k/2 of the position
+      K v[E];
+      if (tm < 32) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = eu_shfl_xor(key[E - 1 - e], tm);
+      } else {
+        exchange(t ^ tm, true, v);
+      }
+      keep(v, lower);
+    }
+#pragma unroll
+    for (int lj = lk - 2; lj >= 0; --lj) {
+      const int j = 1 << lj;
+      if (j < E) {
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          if ((e ^ j) > e) cmpx(e, e ^ j);
+      } else {
+        const int tj = j / E;
+        const bool lower = (t & tj) == 0;
+        K v[E];
+        if (tj < 32) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) v[e] = eu_shfl_xor(key[e], tj);
+        } else {
+          exchange(t ^ tj, false, v);
+        }
+        keep(v, lower);
+      }
+    }
+  }
+}
+
 template <typename T, int NT>
 struct EuBlock {
   static constexpr int E = 16;
   using K = typename BitsT<T>::type;
-  using Sort = cub::BlockRadixSort<K, NT, E, cub::NullType, 4>;
-  // CUB's temp storage, then (after the sort) the padded sorted keys in the
-  // same bytes, then the chunk sums
-  static constexpr size_t kKeys = (static_cast<size_t>(NT) * E * 33 / 32 * sizeof(K) + 15) & ~size_t(15);
-  static constexpr size_t kTmp = (sizeof(typename Sort::TempStorage) + 15) & ~size_t(15);
-  static constexpr size_t kUnion = kTmp > kKeys ? kTmp : kKeys;
+  // the padded keys (the sort's exchange buffer, then the sorted column),
+  // then the chunk sums
+  static constexpr size_t kUnion = (static_cast<size_t>(NT) * E * 33 / 32 * sizeof(K) + 15) & ~size_t(15);
   static constexpr size_t kSmem = kUnion + static_cast<size_t>(NT) * E / kEuChunk * sizeof(DD);
 };
 
@@ -320,8 +407,7 @@ __global__ void __launch_bounds__(NT) k_eu_sort_block(T* __restrict__ mags, int6
   constexpr int E = Cfg::E;
   using K = typename Cfg::K;
   extern __shared__ __align__(16) unsigned char eu_blk_smem[];
-  typename Cfg::Sort::TempStorage& tmp = *reinterpret_cast<typename Cfg::Sort::TempStorage*>(eu_blk_smem);
-  K* S = reinterpret_cast<K*>(eu_blk_smem);  // aliases tmp once the sort is done
+  K* S = reinterpret_cast<K*>(eu_blk_smem);
   DD* cs = reinterpret_cast<DD*>(eu_blk_smem + Cfg::kUnion);
   const int tid = threadIdx.x;
   const int64_t j = blockIdx.x;
@@ -332,8 +418,9 @@ __global__ void __launch_bounds__(NT) k_eu_sort_block(T* __restrict__ mags, int6
     const int i = e * NT + tid;  // striped, coalesced
     key[e] = i < n ? abs_bits(col[i]) : K(0);  // padding: 0 sorts last
   }
-  typename Cfg::Sort(tmp).SortDescending(key, 0, static_cast<int>(sizeof(K) * 8 - 1));  // sign bit always clear
-  __syncthreads();  // temp storage dead: reuse it for the keys
+  // (the unsorted keys' arrangement does not matter: taken as blocked)
+  eu_bitonic_desc<K, NT>(key, S);
+  __syncthreads();  // the last exchange's reads are done: S takes the sorted keys
   auto pad = [](int i) { return i + (i >> 5); };
   // chunk sums straight from the registers: thread t holds ranks 16t ..
   // 16t + 15 (padding keys are 0), chunk c = threads 2c, 2c + 1
