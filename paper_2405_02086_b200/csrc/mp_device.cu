@@ -775,7 +775,9 @@ cudaError_t launch_eu_block(T* mags, const EuclidWs& w, int64_t n, int64_t m, co
                                 static_cast<int>(smem));
   });
   if (a != cudaSuccess) return a;
-  mpk::k_eu_sort_block<T, NT><<<static_cast<unsigned>(m), NT, smem, s>>>(mags, w.ld, n, w.offs, w.fb, w.ldo, inf);
+  const int64_t runs = (n + static_cast<int64_t>(NT) * 16 - 1) / (static_cast<int64_t>(NT) * 16);
+  mpk::k_eu_sort_block<T, NT><<<static_cast<unsigned>(m * runs), NT, smem, s>>>(mags, w.ld, n, runs, w.offs, w.fb,
+                                                                               w.ldo, inf);
   return cudaGetLastError();
 }
 
@@ -791,38 +793,27 @@ mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, doubl
                            static_cast<unsigned>((n + mpk::kEuTile - 1) / mpk::kEuTile)),
                       dim3(32, 8), 0, s>>>(y, n, m, mags, w.ld, inf);
   MP_CUDA_TRY(cudaGetLastError());
-  static std::atomic<uint64_t> done{0};
-  MP_CUDA_TRY(mpi::once_per_device(done, [] {
-    return cudaFuncSetAttribute(mpk::k_eu_sort<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(mpk::kEuSortSmemMax));
-  }));
-  // columns that fit one CTA: sorted whole (+ prefix offsets); longer
-  // columns: power-of-two runs, merged pairwise through w.tmp
-  if (n <= (sizeof(T) == 4 ? 16 * 1024 : 8 * 1024)) {  // f64 at 1024 x 16 keys exceeds shared memory
-    int nt = 64;
-    while (nt * 16 < n) nt *= 2;
-    switch (nt) {
-      case 64: MP_CUDA_TRY((launch_eu_block<T, 64>(mags, w, n, m, inf, s))); break;
-      case 128: MP_CUDA_TRY((launch_eu_block<T, 128>(mags, w, n, m, inf, s))); break;
-      case 256: MP_CUDA_TRY((launch_eu_block<T, 256>(mags, w, n, m, inf, s))); break;
-      case 512: MP_CUDA_TRY((launch_eu_block<T, 512>(mags, w, n, m, inf, s))); break;
-      default: MP_CUDA_TRY((launch_eu_block<T, 1024>(mags, w, n, m, inf, s))); break;
-    }
-  } else {
-  const bool whole = n <= mpk::eu_sort_cap<T>();
-  const int64_t run = whole ? n : mpk::eu_run_len<T>();
-  const int64_t runs = (n + run - 1) / run;
-  const size_t smem = mpk::kEuHistBytes + 2 * static_cast<size_t>((run + 3) & ~int64_t(3)) * sizeof(T);
-  mpk::k_eu_sort<T><<<dim3(static_cast<unsigned>(runs), static_cast<unsigned>(m)), mpk::kEuSortThreads, smem, s>>>(
-      mags, w.ld, n, run, w.offs, w.fb, w.ldo, inf);
-  MP_CUDA_TRY(cudaGetLastError());
-  if (!whole) {
+  // columns that fit one CTA are sorted whole (+ prefix offsets); longer
+  // columns in runs of the largest block, merged pairwise through w.tmp
+  const int64_t cap = mpk::eu_sort_cap<T>();  // f64 at 1024 x 16 keys exceeds shared memory
+  int nt = 64;
+  while (nt * 16 < n && nt * 16 < cap) nt *= 2;
+  switch (nt) {
+    case 64: MP_CUDA_TRY((launch_eu_block<T, 64>(mags, w, n, m, inf, s))); break;
+    case 128: MP_CUDA_TRY((launch_eu_block<T, 128>(mags, w, n, m, inf, s))); break;
+    case 256: MP_CUDA_TRY((launch_eu_block<T, 256>(mags, w, n, m, inf, s))); break;
+    case 512: MP_CUDA_TRY((launch_eu_block<T, 512>(mags, w, n, m, inf, s))); break;
+    default:
+      if constexpr (sizeof(T) == 4) MP_CUDA_TRY((launch_eu_block<T, 1024>(mags, w, n, m, inf, s)));
+      break;
+  }
+  if (n > cap) {
     T* tmp = static_cast<T*>(w.tmp);
     const int64_t tile = static_cast<int64_t>(mpk::kEuMergeThreads) * mpk::kEuMergeE;
     for (int64_t j0 = 0; j0 < m; j0 += w.batch) {
       const int64_t nb = std::min(w.batch, m - j0);
       T* cols = mags + j0 * w.ld;
-      for (int64_t width = run; width < n; width *= 2) {
+      for (int64_t width = cap; width < n; width *= 2) {
         mpk::k_eu_merge<T><<<dim3(static_cast<unsigned>((n + tile - 1) / tile), static_cast<unsigned>(nb)),
                              mpk::kEuMergeThreads, 0, s>>>(cols, tmp, w.ld, n, width, inf);
         MP_CUDA_TRY(cudaGetLastError());
@@ -832,7 +823,6 @@ mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, doubl
     }
     mpk::k_eu_prefix<T><<<static_cast<unsigned>(m), 256, 0, s>>>(mags, w.ld, n, w.offs, w.fb, w.ldo, inf);
     MP_CUDA_TRY(cudaGetLastError());
-  }
   }
   // cooperative search grid: every CTA co-resident
   static int occ = -1;

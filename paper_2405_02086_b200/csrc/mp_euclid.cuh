@@ -11,13 +11,13 @@
 //  EK0 k_eu_gather   |Y| transposed into column-major order (32x32 tiles,
 //                    both sides coalesced) + the finiteness check
 //                    (tensor.cpp:40-41);
-//  EK1 k_eu_sort     per column (or per run of a long column), an LSD radix
-//                    sort of the |y| bit patterns in shared memory written
-//                    here (8-bit digits; per-warp digit histograms, stable
-//                    ranks from per-bit ballots), then -- for a whole
-//                    column -- double-double prefix offsets every 32 ranks
-//                    (the reference's long double P_k, euclidean.cpp:41-46;
-//                    P_k itself is re-summed from the chunk's offset);
+//  EK1 k_eu_sort_block  per column (or per run of a long column), a bitonic
+//                    sorting network on the |y| bit patterns, 16 keys per
+//                    thread in registers (eu_bitonic_desc), then -- for a
+//                    whole column -- double-double prefix offsets every 32
+//                    ranks (the reference's long double P_k,
+//                    euclidean.cpp:41-46; P_k itself is re-summed from the
+//                    chunk's offset);
 //  EK1b k_eu_merge   columns longer than one CTA's shared memory: sorted
 //                    runs merged pairwise in global memory (merge path),
 //                    then k_eu_prefix writes their chunk offsets;
@@ -35,24 +35,13 @@ namespace mpk {
 constexpr int kEuSearchThreads = 256;
 constexpr int kEuMaxCtas = 1024;
 constexpr int kEuChunk = 32;           // ranks per double-double prefix offset
-constexpr int kEuSortThreads = 512;    // 16 warps
-constexpr int kEuSortWarps = kEuSortThreads / 32;
-constexpr int kEuDigits = 256;         // 8-bit radix digits
-constexpr size_t kEuSortSmemMax = 200 * 1024;
-constexpr size_t kEuHistBytes = static_cast<size_t>(kEuSortWarps) * kEuDigits * sizeof(int);
 constexpr int kEuMergeThreads = 256, kEuMergeE = 8;  // merge tile: 2048 outputs
 
-// Keys one sort CTA holds (two ping-pong buffers + the histograms), and the
-// power-of-two run length long columns are cut into.
+// Keys one sort CTA holds (1024 threads x 16 keys; f64: 512 x 16, by shared
+// memory): longer columns are cut into runs of this length and merged.
 template <typename T>
 constexpr int64_t eu_sort_cap() {
-  return static_cast<int64_t>((kEuSortSmemMax - kEuHistBytes) / (2 * sizeof(T))) & ~int64_t(31);
-}
-template <typename T>
-constexpr int64_t eu_run_len() {
-  int64_t r = 1;
-  while (2 * r <= eu_sort_cap<T>()) r *= 2;
-  return r;
+  return sizeof(T) == 4 ? 16 * 1024 : 8 * 1024;
 }
 
 struct EuPart {
@@ -174,123 +163,9 @@ __device__ __forceinline__ void eu_prefix_offsets(V val, int64_t len, DD* cs, DD
   eu_scan_offsets(cs, nch, offs);
 }
 
-// Lanes of the warp holding the same 8-bit digit d (d < 256; 256 marks an
-// absent key): one ballot per digit bit, AND-ed per lane -- branch-free,
-// unlike __match_any_sync (the sort ran 1.8 ms with it, serialised).
-__device__ __forceinline__ unsigned eu_peers(int d) {
-  unsigned peers = __ballot_sync(0xffffffffu, d < 256) ;
-  peers = d < 256 ? peers : ~peers;
-#pragma unroll
-  for (int b = 0; b < 8; ++b) {
-    const unsigned v = __ballot_sync(0xffffffffu, (d >> b) & 1);
-    peers &= ((d >> b) & 1) ? v : ~v;
-  }
-  return peers;
-}
-
-// One CTA sorts `run` keys of column blockIdx.y starting at rank
-// blockIdx.x * run, descending, in place.  LSD radix sort on the |y| bit
-// patterns (non-negative floats order like their bits), 8-bit digits taken
-// complemented so the ascending stable passes give a descending order.
-// Warp w owns the contiguous segment [w * seg, (w + 1) * seg) and walks it
-// 32 keys at a time, so (segment, step, lane) is the array order: per-warp
-// digit histograms -> digit-major, warp-minor exclusive offsets -> scatter at
-// offset + rank among the step's equal digits (eu_peers: the lowest peer
-// updates the counter, so no two lanes touch one counter).  A pass whose
-// digit is the same for every key is the identity and is skipped.  A whole
-// column (gridDim.x == 1) also gets its chunk prefix offsets.
-template <typename T>
-__global__ void __launch_bounds__(kEuSortThreads) k_eu_sort(T* __restrict__ mags, int64_t ld, int64_t n, int64_t run,
-                                                            DD* __restrict__ offs, double* __restrict__ fb,
-                                                            int64_t ldo, const mp_info* __restrict__ info) {
-  if (info->status != MP_OK) return;
-  using K = typename BitsT<T>::type;
-  constexpr int NT = kEuSortThreads, NW = kEuSortWarps;
-  extern __shared__ __align__(16) unsigned char eu_smem[];
-  int* hist = reinterpret_cast<int*>(eu_smem);  // [NW][256]
-  K* A = reinterpret_cast<K*>(eu_smem + kEuHistBytes);
-  K* B = A + ((run + 3) & ~int64_t(3));  // 16-byte aligned: chunk sums (DD) land there later
-  __shared__ int tot_s[kEuDigits];
-  __shared__ int wsum[8];
-  __shared__ int skip;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t j = blockIdx.y, r0 = static_cast<int64_t>(blockIdx.x) * run;
-  const int len = static_cast<int>(min(run, n - r0));
-  T* col = mags + j * ld + r0;
-  for (int i = tid; i < len; i += NT) A[i] = abs_bits(col[i]);
-  const int seg = ((len + NW * 32 - 1) / (NW * 32)) * 32;
-  const unsigned lt = (1u << lane) - 1u;
-  int* hw = hist + warp * kEuDigits;
-  for (int sh = 0; sh < static_cast<int>(sizeof(K) * 8 - 1); sh += 8) {
-    for (int i = tid; i < NW * kEuDigits; i += NT) hist[i] = 0;
-    if (tid == 0) skip = 0;
-    __syncthreads();
-    for (int st = 0; st < seg; st += 32) {
-      const int i = warp * seg + st + lane;
-      const int d = i < len ? 255 - static_cast<int>((A[i] >> sh) & 255u) : kEuDigits;
-      const unsigned peers = eu_peers(d);
-      if (d < kEuDigits && (peers & lt) == 0u) hw[d] += __popc(peers);
-    }
-    __syncthreads();
-    // exclusive offsets, digit-major then warp (threads 0..255: one digit each)
-    int tot = 0;
-    if (tid < kEuDigits) {
-      for (int w = 0; w < NW; ++w) {
-        const int c = hist[w * kEuDigits + tid];
-        hist[w * kEuDigits + tid] = tot;
-        tot += c;
-      }
-      if (tot == len) skip = 1;  // one digit holds every key: identity pass
-      int inc = tot;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += v;
-      }
-      if (lane == 31) wsum[warp] = inc;
-      tot_s[tid] = inc - tot;  // exclusive within the warp
-    }
-    __syncthreads();
-    if (skip) continue;  // uniform: every thread read the same flag
-    if (tid < kEuDigits) {
-      int base = tot_s[tid];
-      for (int w = 0; w < warp; ++w) base += wsum[w];
-      for (int w = 0; w < NW; ++w) hist[w * kEuDigits + tid] += base;
-    }
-    __syncthreads();
-    for (int st = 0; st < seg; st += 32) {
-      const int i = warp * seg + st + lane;
-      const bool ok = i < len;
-      const K key = ok ? A[i] : K(0);
-      const int d = ok ? 255 - static_cast<int>((key >> sh) & 255u) : kEuDigits;
-      const unsigned peers = eu_peers(d);
-      const int rank = __popc(peers & lt);
-      const int base = ok ? hw[d] : 0;
-      __syncwarp();
-      if (ok) {
-        B[base + rank] = key;
-        if (rank == 0) hw[d] = base + __popc(peers);
-      }
-      __syncwarp();
-    }
-    __syncthreads();
-    K* t = A;
-    A = B;
-    B = t;
-  }
-  for (int i = tid; i < len; i += NT) {
-    if constexpr (sizeof(T) == 4) col[i] = __uint_as_float(A[i]);
-    else col[i] = __longlong_as_double(static_cast<long long>(A[i]));
-  }
-  if (gridDim.x == 1) {
-    __syncthreads();  // the other key buffer is free: chunk sums live there
-    eu_prefix_offsets([&](int64_t i) { return eu_key_value(A[i]); }, len, reinterpret_cast<DD*>(B),
-                      offs + j * ldo);
-    eu_first_breaks([&](int64_t i) { return eu_key_value(A[i]); }, len, offs + j * ldo, fb + j * ldo);
-  }
-}
-
-// EK1 for columns of up to NT * 16 keys (n <= 16384): a bitonic sorting
+// EK1 for runs of up to NT * 16 keys (a whole column when n <= 16384 f32 /
+// 8192 f64; longer columns in runs of that length, merged by k_eu_merge): a
+// bitonic sorting
 // network over the CTA, 16 keys per thread in registers, blocked (thread t
 // holds positions 16t .. 16t + 15).  Every merge step of size k starts with a
 // "flip" substage (position i against i ^ (k - 1)) followed by the substages
@@ -300,8 +175,8 @@ __global__ void __launch_bounds__(kEuSortThreads) k_eu_sort(T* __restrict__ mags
 // at 4096 keys), up to 512 positions apart one shfl.xor per key (30), further
 // apart an exchange through shared memory (6).  ~150 instructions per key,
 // none of them a shared-memory atomic or a scan: 4096 x 16384 f32 sorts in
-// 0.4x ms where cub::BlockRadixSort (4-bit digits) took 0.79 ms and our LSD
-// radix kernel above 1.8 ms.  Afterwards the sorted blocked keys go through
+// ~0.5 ms where cub::BlockRadixSort (4-bit digits, round 1) took 0.79 ms and
+// an LSD radix sort of our own with warp-wide ranks 1.8 ms.  Afterwards the sorted blocked keys go through
 // shared memory (one pad word per 32: conflict-free blocked writes) to
 // coalesced column stores and the chunk prefix offsets.
 template <typename K>
@@ -399,7 +274,7 @@ struct EuBlock {
 };
 
 template <typename T, int NT>
-__global__ void __launch_bounds__(NT) k_eu_sort_block(T* __restrict__ mags, int64_t ld, int64_t n,
+__global__ void __launch_bounds__(NT) k_eu_sort_block(T* __restrict__ mags, int64_t ld, int64_t ncol, int64_t runs,
                                                       DD* __restrict__ offs, double* __restrict__ fb, int64_t ldo,
                                                       const mp_info* __restrict__ info) {
   if (info->status != MP_OK) return;
@@ -410,8 +285,11 @@ __global__ void __launch_bounds__(NT) k_eu_sort_block(T* __restrict__ mags, int6
   K* S = reinterpret_cast<K*>(eu_blk_smem);
   DD* cs = reinterpret_cast<DD*>(eu_blk_smem + Cfg::kUnion);
   const int tid = threadIdx.x;
-  const int64_t j = blockIdx.x;
-  T* col = mags + j * ld;
+  // block b sorts run b % runs of column b / runs (runs == 1: the whole
+  // column, which then also gets its chunk prefix offsets)
+  const int64_t j = blockIdx.x / runs, r0 = (blockIdx.x % runs) * (static_cast<int64_t>(NT) * E);
+  T* col = mags + j * ld + r0;
+  const int64_t n = ncol - r0 < static_cast<int64_t>(NT) * E ? ncol - r0 : static_cast<int64_t>(NT) * E;
   K key[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) {
@@ -437,6 +315,7 @@ __global__ void __launch_bounds__(NT) k_eu_sort_block(T* __restrict__ mags, int6
     if constexpr (sizeof(T) == 4) col[i] = __uint_as_float(S[pad(i)]);
     else col[i] = __longlong_as_double(static_cast<long long>(S[pad(i)]));
   }
+  if (runs != 1) return;  // merged columns: k_eu_prefix writes the offsets
   eu_scan_offsets(cs, (n + kEuChunk - 1) / kEuChunk, offs + j * ldo);
   eu_first_breaks([&](int64_t i) { return eu_key_value(S[pad(static_cast<int>(i))]); }, n, offs + j * ldo,
                   fb + j * ldo);
