@@ -12,7 +12,10 @@ import numpy as np
 import torch
 
 import paper_2405_02086_b200 as mp
-from paper_2405_02086_b200 import _capi, datagen
+from paper_2405_02086_b200 import _build, _capi, datagen
+
+if os.environ.get("MP_B200_LIB"):  # A/B runs: a variant build (scripts/ab_build.sh)
+    _build.LIB = os.environ["MP_B200_LIB"]
 from oracle import oracle as O
 
 L = _capi.lib()
