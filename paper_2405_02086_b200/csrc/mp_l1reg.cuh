@@ -391,9 +391,6 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
       for (int par = 0, it = 0; it < 4 * 1024; par ^= 1, ++it) {
         ++npass;
         nx += xp;
-#if MP_L1_CYCLES == 5
-        const long long cq0 = clock64();
-#endif
         // Pieces outer, columns inner: each piece (a shared-memory load for the
         // hybrid part) is read once per pass and feeds C4 independent chains;
         // every column still sums its pieces in ascending i.
@@ -445,13 +442,7 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
           const RegPart<T> wr = reg_reduce<C4, P>(a, lane);
           if (reg_writer<T, P>(lane)) wx[par][warp][reg_col<T, P>(lane)] = wr;
         }
-#if MP_L1_CYCLES == 5
-        const long long cq1 = clock64();
-#endif
         __syncthreads();
-#if MP_L1_CYCLES == 5
-        const long long cq2 = clock64();
-#endif
         if (lane < W && lv) {
           // column totals over the warps, in warp order
           RegPart<T> tot;
@@ -528,14 +519,6 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
 #pragma unroll
         for (int c = 0; c < C4; ++c) thr[c] = __shfl_sync(0xffffffffu, tl, pc + c);
         const unsigned lvb = __ballot_sync(0xffffffffu, lv);
-#if MP_L1_CYCLES == 5
-        {
-          const long long cq3 = clock64();
-          if (xp) cyx += cq1 - cq0; else cyw += cq1 - cq0;
-          cya += cq3 - cq2;
-          cyp += cq2 - cq1;
-        }
-#endif
         if (lvb == 0u) break;
         xp = xp || __ballot_sync(0xffffffffu, lv && ex) != 0u;
       }
@@ -656,7 +639,7 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
       // the next strip's half lands in the same buffer
       if (need_store) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
-#if defined(MP_L1_CYCLES) && MP_L1_CYCLES != 5
+#ifdef MP_L1_CYCLES
       cyx += clock64() - ck2;
 #endif
       // up to four store groups: each group's boxes reload as soon as the
@@ -707,11 +690,9 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
 #ifdef MP_L1_CYCLES
     {
       const long long ck3 = clock64();
-#if MP_L1_CYCLES != 5
       cyw += ck1 - ck0;
       cyp += ck2 - ck1;
       cya += ck3 - ck2;
-#endif
     }
 #endif
     if (!more) break;
