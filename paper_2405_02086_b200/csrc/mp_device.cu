@@ -781,6 +781,8 @@ cudaError_t launch_eu_block(T* mags, const EuclidWs& w, int64_t n, int64_t m, co
   return cudaGetLastError();
 }
 
+constexpr int64_t kEuWarpSearchMaxCols = 4096;
+
 template <typename T>
 mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, double eta, double* budgets,
                       mp_info* info, unsigned flags, const EuclidWs& w, cudaStream_t s) {
@@ -824,12 +826,20 @@ mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, doubl
     mpk::k_eu_prefix<T><<<static_cast<unsigned>(m), 256, 0, s>>>(mags, w.ld, n, w.offs, w.fb, w.ldo, inf);
     MP_CUDA_TRY(cudaGetLastError());
   }
-  // cooperative search grid: every CTA co-resident
-  static int occ = -1;
-  if (occ < 0) MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mpk::k_eu_search<T>,
-                                                                          mpk::kEuSearchThreads, 0));
-  int G = static_cast<int>(std::min<int64_t>((m + mpk::kEuSearchThreads - 1) / mpk::kEuSearchThreads,
-                                             static_cast<int64_t>(sm_count()) * std::max(1, std::min(occ, 2))));
+  // cooperative search grid: every CTA co-resident; a warp per column up to
+  // kEuWarpSearchMaxCols columns, a thread per column beyond
+  const bool warp = m <= kEuWarpSearchMaxCols;
+  static int occ_w = -1, occ_t = -1;
+  if (occ_w < 0) {
+    MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_w, mpk::k_eu_search<T, true>,
+                                                              mpk::kEuSearchThreads, 0));
+    MP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, mpk::k_eu_search<T, false>,
+                                                              mpk::kEuSearchThreads, 0));
+  }
+  const int per_cta = warp ? mpk::kEuSearchThreads / 32 : mpk::kEuSearchThreads;
+  int G = static_cast<int>(std::min<int64_t>(
+      (m + per_cta - 1) / per_cta,
+      static_cast<int64_t>(sm_count()) * std::max(1, warp ? occ_w : std::min(occ_t, 2))));
   G = std::max(1, std::min(G, mpk::kEuMaxCtas));
   const T* cm = mags;
   const mpk::DD* co = w.offs;
@@ -839,8 +849,9 @@ mp_status euclid_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, doubl
   mpk::EuScratch* sc = w.sc;
   int64_t ld = w.ld, ldo = w.ldo;
   void* args[] = {&cm, &co, &cf, &n, &m, &ld, &ldo, &eta, &colmax, &u, &coltot, &inf, &sc};
-  MP_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(mpk::k_eu_search<T>), dim3(G),
-                                          dim3(mpk::kEuSearchThreads), args, 0, s));
+  MP_CUDA_TRY(cudaLaunchCooperativeKernel(warp ? reinterpret_cast<const void*>(mpk::k_eu_search<T, true>)
+                                               : reinterpret_cast<const void*>(mpk::k_eu_search<T, false>),
+                                          dim3(G), dim3(mpk::kEuSearchThreads), args, 0, s));
   if (eta == 0.0) {  // the reference returns DenseTensor::zeros (+0.0 everywhere)
     MP_CUDA_TRY(cudaMemsetAsync(x, 0, static_cast<size_t>(n) * m * sizeof(T), s));
   } else {

@@ -470,9 +470,63 @@ struct EuCol {
     if (r.tk1 < 0.0) r.tk1 = r.k == n ? r.pk.hi + r.pk.lo : brk(r.k + 1);  // k = n: the segment ends at P_n
     return r;
   }
+  // The same segment found by a whole warp (every lane calls with the same
+  // column and theta, every lane gets the result): a 32-way search over the
+  // chunks' first breakpoints (two dependent loads for up to 1024 chunks
+  // instead of a bisection's ten), the chunk's 32 ranks in one coalesced
+  // load, P_k by a double-double warp scan and one ballot over the
+  // breakpoints -- a few hundred cycles where the one-thread walk is a chain
+  // of up to 32 dependent double-double additions.
+  __device__ __forceinline__ Seg segment_warp(double theta, int lane) const {
+    const int64_t nch = (n + kEuChunk - 1) / kEuChunk;
+    int64_t lo = 1, hi = nch;  // chunks [0, lo) start at or below theta, chunks [hi, nch) above it
+    while (lo < hi) {
+      const int64_t step = (hi - lo + 31) / 32, idx = lo + lane * step;
+      const bool p = idx < hi && fb[idx] <= theta;  // non-decreasing: a prefix of the lanes
+      const int cnt = __popc(__ballot_sync(0xffffffffu, p));
+      const int64_t nlo = cnt > 0 ? lo + static_cast<int64_t>(cnt - 1) * step + 1 : lo;
+      const int64_t nhi = lo + static_cast<int64_t>(cnt) * step < hi ? lo + static_cast<int64_t>(cnt) * step : hi;
+      lo = nlo;
+      hi = nhi;
+    }
+    const int64_t c0 = lo - 1, k0 = c0 * kEuChunk + 1, ki = k0 + lane;  // lane i: rank k0 + i
+    const double vi = ki <= n ? static_cast<double>(a_[ki - 1]) : 0.0;
+    DD pi{vi, 0.0};  // inclusive double-double scan of the chunk's ranks
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const DD q{__shfl_up_sync(0xffffffffu, pi.hi, o), __shfl_up_sync(0xffffffffu, pi.lo, o)};
+      if (lane >= o) pi = dd_add(q, pi);
+    }
+    pi = dd_add(off[c0], pi);
+    const double ti = ki <= n ? brk_from_a(pi, ki, vi) : 0.0;
+    const int cnt = __popc(__ballot_sync(0xffffffffu, ki <= n && ti <= theta));  // >= 1: t_{k0} <= theta
+    const int src = cnt > 0 ? cnt - 1 : 0;
+    Seg r;
+    r.k = k0 + src;
+    r.pk = DD{__shfl_sync(0xffffffffu, pi.hi, src), __shfl_sync(0xffffffffu, pi.lo, src)};
+    r.tk = __shfl_sync(0xffffffffu, ti, src);
+    const double tnext = __shfl_sync(0xffffffffu, ti, src + 1 < 32 ? src + 1 : 31);
+    if (r.k == n) r.tk1 = r.pk.hi + r.pk.lo;  // the segment ends at P_n
+    else if (src + 1 < 32) r.tk1 = tnext;
+    else r.tk1 = fb[c0 + 1];  // the next chunk's first breakpoint
+    return r;
+  }
+  // P_n by a warp
+  __device__ __forceinline__ double total_warp(int lane) const {
+    const int64_t c0 = (n - 1) / kEuChunk, ki = c0 * kEuChunk + 1 + lane;
+    DD v{ki <= n ? static_cast<double>(a_[ki - 1]) : 0.0, 0.0};
+    v = warp_reduce_dd(v);
+    const DD t = dd_add(off[c0], v);
+    return t.hi + t.lo;
+  }
 };
 
-template <typename T>
+// WARP: one warp per column (segment_warp) -- up to a few thousand columns
+// the search is a latency chain and the warp version is ~3x shorter (1000 x
+// 1000: 130 -> 93 us for the whole projection); beyond that the thread per
+// column wins, the warp scan issues ~6x the double-double arithmetic
+// (4096 x 16384: 176 vs 265 us).
+template <typename T, bool WARP>
 __global__ void __launch_bounds__(kEuSearchThreads)
     k_eu_search(const T* __restrict__ mags, const DD* __restrict__ offs, const double* __restrict__ fbs, int64_t n,
                 int64_t m, int64_t ld, int64_t ldo,
@@ -484,8 +538,13 @@ __global__ void __launch_bounds__(kEuSearchThreads)
   __shared__ DD dscr[32];
   __shared__ double fscr[32];
   __shared__ long long cscr[32];
-  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
-  const int64_t j0 = static_cast<int64_t>(b) * blockDim.x + tid, js = static_cast<int64_t>(G) * blockDim.x;
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  // WARP: columns strided over the grid's warps, lane 0 carries the warp's
+  // partial sums into the block reductions; else over its threads
+  const int64_t j0 = WARP ? static_cast<int64_t>(b) * (blockDim.x / 32) + (tid >> 5)
+                          : static_cast<int64_t>(b) * blockDim.x + tid,
+                js = WARP ? static_cast<int64_t>(G) * (blockDim.x / 32) : static_cast<int64_t>(G) * blockDim.x;
+  const bool lead = !WARP || lane == 0;  // the thread that carries the column's results
 
   // phase 0: l1,inf norm, largest column mass, column maxima
   DD l1{0.0, 0.0};
@@ -493,11 +552,13 @@ __global__ void __launch_bounds__(kEuSearchThreads)
   for (int64_t j = j0; j < m; j += js) {
     const EuCol<T> c{mags + j * ld, offs + j * ldo, fbs + j * ldo, n};
     const double a1 = static_cast<double>(c.a(0));
-    colmax[j] = a1;
-    l1 = dd_add(l1, a1);
-    const double tot = c.total();
-    coltot[j] = tot;  // P_n, read back by every Newton step
-    tmax = fmax(tmax, tot);
+    const double tot = WARP ? c.total_warp(lane) : c.total();
+    if (lead) {
+      colmax[j] = a1;
+      l1 = dd_add(l1, a1);
+      coltot[j] = tot;  // P_n, read back by every Newton step
+      tmax = fmax(tmax, tot);
+    }
   }
   l1 = block_sum_dd(l1, dscr);
   tmax = -block_min(-tmax, fscr);
@@ -536,12 +597,14 @@ __global__ void __launch_bounds__(kEuSearchThreads)
       for (int64_t j = j0; j < m; j += js) {
         if (theta >= coltot[j]) continue;  // inactive column
         const EuCol<T> c{mags + j * ld, offs + j * ldo, fbs + j * ldo, n};
-        const typename EuCol<T>::Seg g = c.segment(theta);
-        const double kd = static_cast<double>(g.k);
-        A = dd_add(A, dd_div_int(g.pk, kd));
-        B = dd_add(B, dd_div_int(DD{1.0, 0.0}, kd));
-        lo = fmax(lo, g.tk);
-        hi = fmin(hi, g.tk1);
+        const typename EuCol<T>::Seg g = WARP ? c.segment_warp(theta, lane) : c.segment(theta);
+        if (lead) {
+          const double kd = static_cast<double>(g.k);
+          A = dd_add(A, dd_div_int(g.pk, kd));
+          B = dd_add(B, dd_div_int(DD{1.0, 0.0}, kd));
+          lo = fmax(lo, g.tk);
+          hi = fmin(hi, g.tk1);
+        }
       }
       A = block_sum_dd(A, dscr);
       B = block_sum_dd(B, dscr);
@@ -589,12 +652,14 @@ __global__ void __launch_bounds__(kEuSearchThreads)
     } else if (mode == 1 || theta >= coltot[j]) {
       u = 0.0;
     } else {
-      const typename EuCol<T>::Seg g = c.segment(theta);
+      const typename EuCol<T>::Seg g = WARP ? c.segment_warp(theta, lane) : c.segment(theta);
       const DD d = dd_div_int(dd_sub(g.pk, DD{theta, 0.0}), static_cast<double>(g.k));
       u = fmax(0.0, d.hi + d.lo);
     }
-    budgets[j] = u;
-    zc += u == 0.0;
+    if (lead) {
+      budgets[j] = u;
+      zc += u == 0.0;
+    }
   }
   zc = block_count(zc, cscr);
   if (tid == 0) sc->zero[b] = zc;
