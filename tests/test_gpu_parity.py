@@ -409,6 +409,30 @@ def test_device_api_graph_determinism_inplace():
         assert torch.equal(a.view(torch.int32), b.view(torch.int32))  # run-to-run bitwise
 
 
+@pytest.mark.parametrize("n,m,dt", [(4096, 1024, "float32"), (3000, 512, "float32"), (4096, 256, "float64"),
+                                    (6000, 128, "float64")])
+def test_l11_inplace_on_split_apply_strips(n, m, dt):
+    """l1,1 in place (x is y) on the 256 / 512-thread TMA strips, whose apply
+    rewrites the register pieces in place and reloads them for the next
+    strip: same bytes as out of place, and parity with the oracle."""
+    import torch
+    rng = np.random.default_rng(n + m)
+    scale = np.exp(rng.normal(size=m))  # zeroed, projected and feasible columns
+    y_h = (rng.normal(size=(n, m)) * scale).astype(dt)
+    y = torch.from_numpy(y_h).cuda()
+    eta = 0.2 * O.matrix_pq_norm(y_h.astype(np.float64), "1", "1")
+    proj = mp.BilevelProjector(n, m, dt, "1", "1")
+    x = torch.empty_like(y)
+    proj(y, x, eta)
+    z = proj.info().zero_columns
+    y2 = y.clone()
+    proj(y2, y2, eta)
+    torch.cuda.synchronize()
+    it = torch.int32 if dt == "float32" else torch.int64
+    assert torch.equal(x.view(it), y2.view(it))
+    check_bilevel(x.cpu().numpy(), y_h, oracle_bilevel(y_h, eta, "1", "1"), "1", zero_cols_gpu=z)
+
+
 def test_idempotence_full_size():
     """Project, then project the result at eta(1+1e-6): identical bytes."""
     y = datagen.config_input(2, scale=0.5)
