@@ -733,8 +733,6 @@ struct EuclidWs {
   mpk::EuScratch* sc;
 };
 
-int pow2_at_least(int64_t n);
-
 template <typename T>
 int64_t eu_merge_batch(int64_t n, int64_t m, int64_t ld) {
   if (n <= mpk::eu_sort_cap<T>()) return 0;
@@ -758,12 +756,6 @@ EuclidWs carve_euclid(Carve& c, mp_dtype dt, int64_t n, int64_t m) {
   w.colp = c.take<double>(m);
   w.sc = c.take<mpk::EuScratch>(1);
   return w;
-}
-
-int pow2_at_least(int64_t n) {
-  int p = 1;
-  while (p < n) p <<= 1;
-  return p;
 }
 
 template <typename T, int NT>
