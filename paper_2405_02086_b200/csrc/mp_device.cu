@@ -217,9 +217,31 @@ cudaError_t launch_colnorm(int q, int vec, const T* y, int64_t n, int64_t m, voi
   return launch_colnorm_v<T, 1>(q, y, n, m, out, g, s, ncopy);
 }
 
+// The apply pass can run the outer projection itself (k_apply FUSE) when one
+// column tile holds the whole norm vector -- and pays when the grid is small:
+// every CTA repeats the projection (a few block reductions over L2-resident
+// norms, ~3 us at the head of the kernel) where a K2 launch costs ~4 us of
+// latency chain.  Measured K1 start to K3 end: 300 x 900 11.3 -> 9.7 us,
+// 1000 x 1000 13.1 -> 12.0, 5000 x 1024 25.9 -> 25.1; but 20000 x 512 26.1 ->
+// 27.3 and 65536 x 256 31.2 -> 33.5 (thousands of CTAs fold the maxima's
+// copies and repeat the projection), hence the element cap.
+constexpr int64_t kFuseMaxElements = int64_t(6) << 20;
+bool apply_fusable(int vec, int64_t n, int64_t m) {
+  return (m + vec - 1) / vec <= mpk::kThreads && n * m <= kFuseMaxElements;
+}
+
 template <typename T, int VEC, int Q, int U>
 cudaError_t launch_apply_qu(const T* y, T* x, int64_t n, int64_t m, const mpk::ApplyCols& A, bool derive,
-                            const mp_info* info, unsigned flags, cudaStream_t s) {
+                            const mp_info* info, unsigned flags, cudaStream_t s, bool fuse = false) {
+  if (fuse) {  // one tile of whole warps (the core's block reductions)
+    const int tf = (threads_for(VEC, m) + 31) & ~31;
+    const void* ff = reinterpret_cast<const void*>(mpk::k_apply<T, VEC, Q, U, true, true>);
+    Grid gf = plan_grid(VEC, n, m, occupancy(ff, tf));
+    gf.threads = tf;
+    dim3 gridf(1, static_cast<unsigned>(gf.nrb));
+    return launch_pdl(mpk::k_apply<T, VEC, Q, U, true, true>, gridf, dim3(tf), 0, s, y, x, n, m,
+                      kRowInterleave ? n / gf.nrb : gf.rpb, kRowInterleave, A, info, flags);
+  }
   const int t = threads_for(VEC, m);
   const void* fn = derive ? reinterpret_cast<const void*>(mpk::k_apply<T, VEC, Q, U, true>)
                           : reinterpret_cast<const void*>(mpk::k_apply<T, VEC, Q, U, false>);
@@ -239,31 +261,33 @@ cudaError_t launch_apply_qu(const T* y, T* x, int64_t n, int64_t m, const mpk::A
 // HBM round trip for their few rows, config 1 K3 3.8 -> 2.8 us).
 template <typename T, int VEC, int Q>
 cudaError_t launch_apply_q(const T* y, T* x, int64_t n, int64_t m, const mpk::ApplyCols& A, bool derive,
-                           const mp_info* info, unsigned flags, cudaStream_t s) {
+                           const mp_info* info, unsigned flags, cudaStream_t s, bool fuse) {
   if constexpr (Q == mpk::kInf) {
     const int t = threads_for(VEC, m);
     const Grid g8 = plan_grid(VEC, n, m, occupancy(reinterpret_cast<const void*>(mpk::k_apply<T, VEC, Q, 8, true>), t));
-    if (n / g8.nrb >= 16) return launch_apply_qu<T, VEC, Q, 8>(y, x, n, m, A, derive, info, flags, s);
+    if (n / g8.nrb >= 16) return launch_apply_qu<T, VEC, Q, 8>(y, x, n, m, A, derive, info, flags, s, fuse);
   }
-  return launch_apply_qu<T, VEC, Q, 4>(y, x, n, m, A, derive, info, flags, s);
+  return launch_apply_qu<T, VEC, Q, 4>(y, x, n, m, A, derive, info, flags, s, fuse);
 }
 
 template <typename T, int VEC>
 cudaError_t launch_apply_v(int q, const T* y, T* x, int64_t n, int64_t m, const mpk::ApplyCols& A, bool derive,
-                           const mp_info* info, unsigned flags, cudaStream_t s) {
-  if (q == mpk::kInf) return launch_apply_q<T, VEC, mpk::kInf>(y, x, n, m, A, derive, info, flags, s);
-  return launch_apply_q<T, VEC, mpk::kL2>(y, x, n, m, A, derive, info, flags, s);
+                           const mp_info* info, unsigned flags, cudaStream_t s, bool fuse) {
+  if (q == mpk::kInf) return launch_apply_q<T, VEC, mpk::kInf>(y, x, n, m, A, derive, info, flags, s, fuse);
+  return launch_apply_q<T, VEC, mpk::kL2>(y, x, n, m, A, derive, info, flags, s, fuse);
 }
 
+// `fuse` (derive only, apply_fusable(vec, m)): A.outer holds the outer
+// projection's arguments and no K2 was launched.
 template <typename T>
 cudaError_t launch_apply(int q, int vec, const T* y, T* x, int64_t n, int64_t m, const mpk::ApplyCols& A,
-                         bool derive, const mp_info* info, unsigned flags, cudaStream_t s) {
+                         bool derive, const mp_info* info, unsigned flags, cudaStream_t s, bool fuse = false) {
   if (vec == 8) {
-    if constexpr (sizeof(T) == 4) return launch_apply_v<T, 8>(q, y, x, n, m, A, derive, info, flags, s);
+    if constexpr (sizeof(T) == 4) return launch_apply_v<T, 8>(q, y, x, n, m, A, derive, info, flags, s, fuse);
   }
-  if (vec == 4) return launch_apply_v<T, 4>(q, y, x, n, m, A, derive, info, flags, s);
-  if (vec == 2) return launch_apply_v<T, 2>(q, y, x, n, m, A, derive, info, flags, s);
-  return launch_apply_v<T, 1>(q, y, x, n, m, A, derive, info, flags, s);
+  if (vec == 4) return launch_apply_v<T, 4>(q, y, x, n, m, A, derive, info, flags, s, fuse);
+  if (vec == 2) return launch_apply_v<T, 2>(q, y, x, n, m, A, derive, info, flags, s, fuse);
+  return launch_apply_v<T, 1>(q, y, x, n, m, A, derive, info, flags, s, fuse);
 }
 
 template <int P>
@@ -474,7 +498,12 @@ mp_status bilevel_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, mp_n
     A.vkind = 1;
   }
   prof_mark(1, s);
-  if (m > mpk::kOuterMaxM) {
+  // Narrow matrices (one column tile): every CTA of the apply pass runs the
+  // outer projection itself, no K2 launch.
+  const bool fuse = derive && q != MP_NORM_L1 && apply_fusable(vec, n, m);
+  if (fuse) {
+    A.outer = oa;
+  } else if (m > mpk::kOuterMaxM) {
     MP_CUDA_TRY(mpk::launch_outer_large(oa, s));
   } else {
     MP_CUDA_TRY(launch_outer(oa, s));
@@ -489,7 +518,7 @@ mp_status bilevel_impl(const T* y, T* x, mp_dtype dt, int64_t n, int64_t m, mp_n
     }
     MP_CUDA_TRY(mpk::launch_l1strip<T>(y, x, n, m, v, u, w.l1, inf, flags, s, dv));
   } else {
-    MP_CUDA_TRY(launch_apply<T>(q, vec, y, x, n, m, A, true, inf, flags, s));
+    MP_CUDA_TRY(launch_apply<T>(q, vec, y, x, n, m, A, true, inf, flags, s, fuse));
   }
   prof_mark(3, s);
   return MP_OK;

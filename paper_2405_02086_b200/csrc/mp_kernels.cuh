@@ -466,6 +466,7 @@ struct OuterArgs {
 // is order-free; all loads in flight) and leave the result in copy 0 for the
 // apply pass.
 constexpr int kInfCopies = 8;
+template <bool STORE = true>
 __device__ __forceinline__ double outer_load_fold(const OuterArgs& a, int64_t i) {
   if (a.vkind == 0) {
     unsigned* b = static_cast<unsigned*>(const_cast<void*>(a.vin));
@@ -475,7 +476,7 @@ __device__ __forceinline__ double outer_load_fold(const OuterArgs& a, int64_t i)
     unsigned mx = c8[0];
 #pragma unroll
     for (int c = 1; c < kInfCopies; ++c) mx = max(mx, c8[c]);
-    b[i] = mx;
+    if (STORE) b[i] = mx;
     return static_cast<double>(__uint_as_float(mx));
   }
   unsigned long long* b = static_cast<unsigned long long*>(const_cast<void*>(a.vin));
@@ -485,7 +486,7 @@ __device__ __forceinline__ double outer_load_fold(const OuterArgs& a, int64_t i)
   unsigned long long mx = c8[0];
 #pragma unroll
   for (int c = 1; c < kInfCopies; ++c) mx = max(mx, c8[c]);
-  b[i] = mx;
+  if (STORE) b[i] = mx;
   return __longlong_as_double(static_cast<long long>(mx));
 }
 
@@ -752,30 +753,35 @@ constexpr int kOuterRegThreads = 1024;
 constexpr int kOuterRegMaxP = 12;
 constexpr int64_t kOuterRegMaxM = static_cast<int64_t>(kOuterRegThreads) * kOuterRegMaxP;
 
-// K2 fast path (m <= 12288): ONE CTA of NT threads (1024; 256 for m <= 2048,
-// where the barriers of the per-pass all-reduce dominate), the vector held in
-// registers (P per thread, compile time), every reduction a single-barrier
-// all-reduce.  The kernel's time is its dependency chain on one SM: a load
-// wave, 1 + passes + 1 block reductions, one double division per pass.
-template <int P, int NT = kOuterRegThreads, bool FOLD = false>
-__global__ void __launch_bounds__(NT, 1) k_outer_reg(OuterArgs a) {
-  pdl_wait();
-  pdl_trigger();
-  tl_begin(2);
-  __shared__ double sb[2][32];
-  __shared__ int cb[2][32];
-  int par = 0;
-  const int tid = threadIdx.x;
+// The outcome of the outer projection of the norm vector.
+struct OuterOutcome {
+  int mode;  // 0 identity, 1 zero, 2 l1 threshold, 3 l2 scale, 4 linf clip
+  double tau, scale;
+  int active, iters, zeros;
+  bool bad;  // a non-finite norm
+};
+
+// The body of the fast path: the CTA's threads hold the vector (element
+// tid + j * blockDim.x in v[j]) and every thread returns the same outcome.
+// Shared by k_outer_reg and by the apply pass of narrow matrices, whose CTAs
+// each run it themselves instead of waiting for a K2 launch (k_apply, FUSE).
+// FOLD: 0 one copy of the norms, 1 fold K1's copies and leave the result in
+// copy 0 (K2), 2 fold without the store (the fused apply pass: thousands of
+// CTAs would write the same words).
+template <int P, int FOLD>
+__device__ __forceinline__ OuterOutcome outer_reg_core(const OuterArgs& a, double (&v)[P], double (*sb)[32],
+                                                       int (*cb)[32], int& par) {
+  const int tid = threadIdx.x, NT = blockDim.x;
   const int m = static_cast<int>(a.m);
   const double eta = a.eta;
-
-  double v[P];
   double s = 0.0;
   int bad = 0;
 #pragma unroll
   for (int j = 0; j < P; ++j) {
     const int i = tid + j * NT;
-    v[j] = (i < m) ? (FOLD ? outer_load_fold(a, i) : outer_load(a, i)) : 0.0;
+    v[j] = (i < m) ? (FOLD == 1 ? outer_load_fold<true>(a, i) : FOLD == 2 ? outer_load_fold<false>(a, i)
+                                                                          : outer_load(a, i))
+                   : 0.0;
   }
   int nzero = 0;
 #pragma unroll
@@ -789,34 +795,23 @@ __global__ void __launch_bounds__(NT, 1) k_outer_reg(OuterArgs a) {
   block_allreduce(s, flags_zeros, sb, cb, par);
   bad = flags_zeros >> 18;
   nzero = flags_zeros & ((1 << 18) - 1);
-  if (bad) {
-    if (tid == 0) {
-      a.info->status = MP_ERR_VALUE;
-      a.info->tau = -1.0;
-      a.info->active = -1;
-      a.info->iterations = 0;
-    }
-    return;
-  }
-
-  int mode = 0;  // 0 identity, 1 zero, 2 l1 threshold, 3 l2 scale, 4 linf clip
-  double tau = -1.0, scale = 1.0;
-  int active = -1, iters = 0;
+  OuterOutcome o{0, -1.0, 1.0, -1, 0, 0, bad != 0};
+  if (bad) return o;
   if (a.p == kInf) {
-    mode = 4;
+    o.mode = 4;
   } else if (a.p == kL2) {
     const double norm = sqrt(s);
     if (!(norm <= eta) && norm != 0.0) {
-      mode = 3;
-      scale = eta / norm;
+      o.mode = 3;
+      o.scale = eta / norm;
     }
   } else if (m > 0 && !(s <= eta)) {
     if (eta == 0.0) {
-      mode = 1;
-      tau = 0.0;
-      active = 0;
+      o.mode = 1;
+      o.tau = 0.0;
+      o.active = 0;
     } else {
-      mode = 2;
+      o.mode = 2;
       unsigned mask = 0;
 #pragma unroll
       for (int j = 0; j < P; ++j)
@@ -836,7 +831,7 @@ __global__ void __launch_bounds__(NT, 1) k_outer_reg(OuterArgs a) {
           mask = keep ? mask : (mask & ~(1u << j));
         }
         block_allreduce(ps, pc, sb, cb, par);
-        ++iters;
+        ++o.iters;
         if (pc == 0) break;  // cannot happen for eta > 0; keep the last set
         S = ps;
         const bool stable = (pc == kprev);
@@ -844,15 +839,58 @@ __global__ void __launch_bounds__(NT, 1) k_outer_reg(OuterArgs a) {
         if (stable) break;
         t = (ps - eta) / static_cast<double>(pc);
       }
-      active = kprev;
-      tau = (S - eta) / static_cast<double>(active);
+      o.active = kprev;
+      o.tau = (S - eta) / static_cast<double>(o.active);
     }
   }
-
-  if (tid == 0) outer_publish(a, mode, tau, scale);
   // Zero columns follow from the outcome (u == 0 <=> v <= tau for the l1
   // threshold, v == 0 for identity / scale / clip); survivors = m - zeros.
-  const int zeros = outer_zero_count(mode, m, active, nzero, eta, scale);
+  o.zeros = outer_zero_count(o.mode, m, o.active, nzero, eta, o.scale);
+  return o;
+}
+
+// What K2 leaves in mp_info (thread 0 of one CTA).
+__device__ __forceinline__ void outer_write_info(mp_info* info, const OuterOutcome& o, int m) {
+  if (o.bad) {
+    info->status = MP_ERR_VALUE;
+    info->tau = -1.0;
+    info->active = -1;
+    info->iterations = 0;
+    return;
+  }
+  info->status = MP_OK;
+  info->tau = o.tau;
+  info->active = o.active;
+  info->iterations = o.iters;
+  info->zero_columns = o.zeros;
+  info->survivors = m - o.zeros;
+}
+
+// K2 fast path (m <= 12288): ONE CTA of NT threads (1024; 256 for m <= 2048,
+// where the barriers of the per-pass all-reduce dominate), the vector held in
+// registers (P per thread, compile time), every reduction a single-barrier
+// all-reduce.  The kernel's time is its dependency chain on one SM: a load
+// wave, 1 + passes + 1 block reductions, one double division per pass.
+template <int P, int NT = kOuterRegThreads, bool FOLD = false>
+__global__ void __launch_bounds__(NT, 1) k_outer_reg(OuterArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  tl_begin(2);
+  __shared__ double sb[2][32];
+  __shared__ int cb[2][32];
+  int par = 0;
+  const int tid = threadIdx.x;
+  const int m = static_cast<int>(a.m);
+  const double eta = a.eta;
+  double v[P];
+  const OuterOutcome o = outer_reg_core<P, FOLD ? 1 : 0>(a, v, sb, cb, par);
+  if (o.bad) {
+    if (tid == 0) outer_write_info(a.info, o, m);
+    return;
+  }
+  const int mode = o.mode;
+  const double tau = o.tau, scale = o.scale;
+  if (tid == 0) outer_publish(a, mode, tau, scale);
   if (a.emit) {
 #pragma unroll
     for (int j = 0; j < P; ++j) {
@@ -877,14 +915,7 @@ __global__ void __launch_bounds__(NT, 1) k_outer_reg(OuterArgs a) {
       }
     }
   }
-  if (tid == 0) {
-    a.info->status = MP_OK;
-    a.info->tau = tau;
-    a.info->active = active;
-    a.info->iterations = iters;
-    a.info->zero_columns = zeros;
-    a.info->survivors = m - zeros;
-  }
+  if (tid == 0) outer_write_info(a.info, o, m);
   tl_end(2);
 }
 
@@ -905,6 +936,7 @@ struct ApplyCols {
   double* u_out;          // DERIVE, nullable
   double* v_out;          // DERIVE, nullable
   mp_info* info_w;        // unused (K2 counts zero columns); kept for ABI of the kernel args
+  OuterArgs outer;        // FUSE: the outer projection's arguments (no K2 launch)
 };
 
 __device__ __forceinline__ double load_norm(const ApplyCols& a, int64_t c) {
@@ -912,18 +944,49 @@ __device__ __forceinline__ double load_norm(const ApplyCols& a, int64_t c) {
                       : static_cast<const double*>(a.v)[c];
 }
 
+// FUSE: column tile == the whole vector (one tile of blockDim.x * VEC >= m
+// columns, blockDim.x a multiple of 32).  Every CTA of the apply pass runs the
+// outer projection itself (outer_reg_core: a few block reductions over norms
+// that sit in L2) instead of waiting for a one-CTA K2 launch: config 4
+// (65536 x 256) K2 was 7 of 36 us, config 1 3.3 of 18 us.  CTA (0, 0) leaves
+// K2's mp_info / OuterParams.  The threshold's f64 sums associate by this
+// kernel's thread layout, so it may differ from a stand-alone K2's by an ulp.
+template <int VEC, int FOLD>
+__device__ __forceinline__ OuterOutcome apply_fused_outer(const ApplyCols& A) {
+  __shared__ double sb[2][32];
+  __shared__ int cb[2][32];
+  int par = 0;
+  double vv[VEC];
+  const OuterOutcome o = outer_reg_core<VEC, FOLD>(A.outer, vv, sb, cb, par);
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    outer_write_info(A.outer.info, o, static_cast<int>(A.outer.m));
+    if (!o.bad) outer_publish(A.outer, o.mode, o.tau, o.scale);
+  }
+  return o;
+}
+
 // l_inf clamp (proj/src/fiber_kernels.cpp:43-49) / l2 scale (:50-55).
 // `dead` packs (all budgets 0) are written as +0 without a read unless
 // MP_FLAG_EXACT_ZERO_SIGN.
 // f32 l2 runs at 4 CTAs per SM (<= 64 registers): 143.4 vs 145.4 us on config 3
 // l1,2 at the 5 CTAs its 48 registers would allow (a grid of fewer row slots).
-template <typename T, int VEC, int Q, int U, bool DERIVE>
+template <typename T, int VEC, int Q, int U, bool DERIVE, bool FUSE = false>
 __global__ void __launch_bounds__(kThreads, (Q == kL2 && sizeof(T) == 4) ? 4 : 0)
     k_apply(const T* __restrict__ y, T* __restrict__ x, int64_t n, int64_t m, int64_t rpb, int interleave,
             ApplyCols A, const mp_info* __restrict__ info, unsigned flags) {
   pdl_wait();
   tl_begin(3);
-  if (info->status != MP_OK) return;
+  OuterParams PF{};  // FUSE: this CTA's own outer projection
+  if constexpr (FUSE) {
+    const OuterOutcome o = A.outer.ncopy > 1 ? apply_fused_outer<VEC, 2>(A) : apply_fused_outer<VEC, 0>(A);
+    if (o.bad) return;
+    PF.mode = o.mode;
+    PF.tau = o.tau;
+    PF.scale = o.scale;
+    PF.eta = A.outer.eta;
+  } else {
+    if (info->status != MP_OK) return;
+  }
   const int64_t c0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * VEC;
   if (c0 >= m) return;
   const RowWalk rw = row_walk(n, rpb, interleave);
@@ -933,10 +996,10 @@ __global__ void __launch_bounds__(kThreads, (Q == kL2 && sizeof(T) == 4) ? 4 : 0
   double pu[VEC];
   bool dead = !(flags & MP_FLAG_EXACT_ZERO_SIGN);
   if constexpr (DERIVE) {
-    const OuterParams P = *A.params;
+    const OuterParams P = FUSE ? PF : *A.params;
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
-      const double vj = load_norm(A, c0 + j);
+      const double vj = (FUSE && A.outer.ncopy > 1) ? outer_load_fold<false>(A.outer, c0 + j) : load_norm(A, c0 + j);
       const double uj = derive_u(P, vj);
       if constexpr (Q == kInf && sizeof(T) == 4) {
         rd[j] = __double2float_rz(uj);
