@@ -182,6 +182,8 @@ def run_reference(args, rank):
                                    "1 per step cycling the 4 radii; time includes the API's own output copy"},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "step_stats": step_stats([1e3 * t for t in per]),
+        # north_star: elements/s beside GB/s (matrix elements projected per second)
+        "elements_per_s": N_ROWS * N_COLS * len(per) / total_t,
     }
     print(json.dumps(line), flush=True)
 
@@ -537,6 +539,8 @@ def run_ours(args, rank, world, local_rank):
             "e2e_dropin": dropin,
             "clocks": clock_info,
             "gpu_launches": 3 * nproj * args.steps,
+            # north_star: elements/s beside GB/s (matrix elements projected per second, device-timed)
+            "elements_per_s": world * N_ROWS * N_COLS * nproj / (ms_per_step * 1e-3),
         }
         print(json.dumps(line), flush=True)
 

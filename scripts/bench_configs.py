@@ -63,7 +63,7 @@ def timed_graph(call, nproj=1):
 def line(name, n_elems, f_surv, ms, cpu_s=None, extra=None, s=4.0):
     b = s * n_elems * (2.0 + f_surv)
     d = {"config": name, "ms": ms, "algo_bytes": b, "GBps": b / (ms * 1e-3) / 1e9, "frac_measured_hbm": b / (ms * 1e-3) / 1e9 / peak,
-         "f_surv": f_surv}
+         "f_surv": f_surv, "elements_per_s": n_elems / (ms * 1e-3)}
     if cpu_s is not None:
         d["cpu_reference_s"] = cpu_s
         d["cpu_reference_GBps"] = b / cpu_s / 1e9
