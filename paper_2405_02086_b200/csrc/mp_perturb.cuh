@@ -60,7 +60,8 @@ __global__ void __launch_bounds__(256)
   if constexpr (V4) {  // f32, 16-byte aligned, count % 4 == 0
     // four quads per thread in flight: the loads are issued before the
     // ~120 instructions of Philox and Box-Muller per quad (one load at a time
-    // left the kernel at 84% of the copy rate)
+    // left the kernel at 84% of the copy rate; two in flight 394 us, four
+    // 363 us, eight 415 us per GiB)
     constexpr int kU = 4;
     float4* x4 = reinterpret_cast<float4*>(x);
     for (; (q + (kU - 1) * stride) * 4 < count; q += kU * stride) {
