@@ -618,8 +618,9 @@ __global__ void __launch_bounds__(NT, kRegThreads / NT)
         }
       }
     } else {
-      // (register-only strips measured 5-20% slower with the split order:
-      // their next strip's loads would start only after all the stores)
+      // (register-only strips measured 5-20% slower with the split order --
+      // their next strip's loads would start only after all the stores -- and
+      // 6-13% slower with in-place stores and the loads lagging 2-4 pieces)
 #pragma unroll
       for (int i = 0; i < NPC; ++i, xq += step, yn += step) {
         if (rb + SL * i >= n) break;
